@@ -1,0 +1,219 @@
+/*
+ * syscd_b200 — C ABI of the B200-native SySCD training epoch.
+ *
+ * The reference (arxiv/paper_1911_07722, pure Python package `syscd`) has no
+ * native FFI; its drop-in boundary for this path is the Python call
+ *     syscd.run_syscd(problem, cfg, f_star)      pkg/src/syscd/solvers.py:337
+ *     syscd.run_solver(problem, cfg, f_star)     pkg/src/syscd/solvers.py:456
+ * The entry points below are what that call decomposes into on a GPU; the
+ * Python package paper_1911_07722_b200 binds them with ctypes (see
+ * INTEGRATION.md for the stub a syscd maintainer would add).  Each function
+ * names the reference code it replaces.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Device pointers are borrowed for the
+ *    duration of the call; no allocation happens on the hot calls (workspace
+ *    is passed in).  `stream` is a cudaStream_t passed as void*.
+ *  - Every function returns a status: SYSCD_OK, SYSCD_EINVAL (configuration
+ *    error -> ValueError, solvers.py:63-79,346-353, partitioning.py:78-106),
+ *    SYSCD_ENONFINITE (-> NonFiniteUpdateError, objective.py:13-14,
+ *    solvers.py:307-308), SYSCD_ECUDA (CUDA/NCCL error -> RuntimeError).
+ *    syscd_last_error() returns a thread-local message for the last failure.
+ *  - No global mutable state besides that message: concurrent calls on
+ *    distinct problems are safe.
+ */
+#ifndef SYSCD_B200_H_
+#define SYSCD_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SYSCD_ABI_VERSION 1
+
+/* status codes */
+#define SYSCD_OK 0
+#define SYSCD_EINVAL 1
+#define SYSCD_ENONFINITE 2
+#define SYSCD_ECUDA 3
+
+/* objective kinds: f(A alpha) + sum_j g_j(alpha_j) */
+#define SYSCD_RIDGE 0          /* squared loss + l2 (objective.py:26,62-63)          */
+#define SYSCD_LOGISTIC 1       /* primal logistic + l2 (objective.py:30,36-42)       */
+#define SYSCD_LASSO 2          /* squared loss + l1             */
+#define SYSCD_SVM_DUAL 3       /* hinge SVM dual, columns y_i x_i (Appendix A)      */
+#define SYSCD_LOGISTIC_DUAL 4  /* logistic dual, columns y_i x_i (Appendix A)       */
+
+int syscd_abi_version(void);
+const char* syscd_last_error(void);
+
+/* ------------------------------------------------------------------------
+ * RNG contract (host).  Bit-exact restatement of
+ *   np.random.default_rng(np.random.SeedSequence(seed, spawn_key=key))
+ * (partitioning.py:30-38) consumed by Generator.permutation
+ * (partitioning.py:95,107,117) and Generator.integers (solvers.py:159-166).
+ * Replaces: RngStream.generator().permutation / .integers.
+ * ------------------------------------------------------------------------ */
+int syscd_rng_permutation(uint64_t seed, const uint64_t* key, int32_t key_len, int64_t n,
+                          int64_t* out);
+int syscd_rng_integers(uint64_t seed, const uint64_t* key, int32_t key_len, int64_t lo,
+                       int64_t hi, int64_t count, int64_t* out);
+
+/* ------------------------------------------------------------------------
+ * Device planning of one or more rounds (the seeded device-side
+ * re-partitioning).  Replaces per round: _worker_bucket_order +
+ * dynamic_repartition (solvers.py:174-178, partitioning.py:99-109) and the
+ * per-bucket permute_within_bucket / iid draws of _surrogate_thread_round
+ * (solvers.py:315-333, partitioning.py:112-117).
+ *
+ * Output per round r (0 <= r < n_rounds, rid = rid0 + r):
+ *   seq[r*seq_stride + i]           store column of the i-th update, the
+ *                                   partitions' sequences laid out back to back
+ *                                   in (local node, thread) order;
+ *   work_prefix[r*(n_parts+1) + p]  start of partition p in seq (exclusive
+ *                                   prefix of the per-partition update counts),
+ *                                   n_parts = n_nodes_local * P.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  uint64_t seed;
+  int64_t n_global;        /* coordinates of the whole problem                    */
+  int32_t bucket_size;     /* B (solvers.py:81-84)                                */
+  int32_t n_nodes_local;   /* node groups planned here                            */
+  int32_t node0;           /* global id k of the first local node                 */
+  int32_t P;               /* threads per node                                    */
+  int32_t T3;              /* buckets per thread per round, -1 = all               */
+  int32_t T4;              /* updates per bucket, -1 = bucket length / B (iid)     */
+  int32_t sampling;        /* 0 = perm, 1 = iid                                   */
+  int32_t repartition;     /* 0 = dynamic, 1 = static                             */
+  const int32_t* node_bucket_ptr;  /* [n_nodes_local+1] host array                */
+  const int32_t* node_buckets;     /* device: global bucket ids per node, in
+                                      static_node_partition order                 */
+  const int64_t* bucket_store_col; /* device: store column of each listed
+                                      bucket's first coordinate                   */
+} syscd_plan_desc;
+
+/* bytes of workspace syscd_plan needs for n_rounds rounds */
+int64_t syscd_plan_workspace_bytes(const syscd_plan_desc* desc, int32_t n_rounds);
+/* upper bound of the per-round update count (size seq_stride >= this) */
+int64_t syscd_plan_max_updates(const syscd_plan_desc* desc);
+int syscd_plan(const syscd_plan_desc* desc, int64_t rid0, int32_t n_rounds, int32_t* seq,
+               int64_t seq_stride, int64_t* work_prefix, void* workspace, int64_t workspace_bytes,
+               void* stream);
+
+/* ------------------------------------------------------------------------
+ * One node-local round on the GPU: every partition of the plan runs its
+ * chain  lin = x_j.(u + a dv) ; alpha_j <- step ; dv += delta x_j  on a
+ * private replica, and the replicas are summed into `partials`
+ * (_surrogate_thread_round solvers.py:289-334 + the intra-node part of
+ * reduce_replicas solvers.py:393).  Dense column-major fp32 store.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  int32_t kind;            /* SYSCD_* objective                                     */
+  int64_t d;               /* shared-vector length (rows)                           */
+  int64_t lda;             /* leading dimension (floats), multiple of 4, >= d       */
+  const float* A;          /* device, store columns                                 */
+  const float* sq;         /* device, column squared norms per store column         */
+  float* alpha;            /* device, model per store column (read/write)           */
+  const float* u;          /* device, lin_vec = grad f(v) (+ drift), length d       */
+  const int32_t* seq;      /* device, one round of syscd_plan output                */
+  const int64_t* work_prefix; /* device, [n_parts+1]                                */
+  int32_t n_parts;
+  double a;                /* surrogate curvature gamma*K*P (solvers.py:359)        */
+  double lam;
+  double n_coords;         /* global coordinate count (dual objectives' 1/n)        */
+  int32_t iid;             /* 1 if coordinates may repeat within a round            */
+  int64_t n_store;         /* columns in the store (L2 residency hint)              */
+  float* partials;         /* device, [n_workers][part_ld] fp32, written here       */
+  int64_t part_ld;
+  int32_t* status;         /* device int, OR-ed with 2 on a non-finite step         */
+} syscd_dense_epoch_args;
+
+/* workers the dense epoch uses for this geometry (partials must hold that many rows) */
+int syscd_dense_epoch_workers(int64_t d, int32_t n_parts, int32_t* n_workers, int32_t* cluster);
+int syscd_dense_epoch(const syscd_dense_epoch_args* e, void* stream);
+
+
+
+/* Sparse CSC store (int64 col_ptr, int32 row_idx, fp32 values); sparse
+ * col_dot / col_axpy of dataset.py:77-78,90-91.  One warp per worker; each
+ * worker's private replica row of dv_work (n_workers x d fp32) must be all-zero
+ * on entry and is all-zero again on return; delta_v (d) receives the sum of
+ * the replicas (zeroed by the call). */
+typedef struct {
+  int32_t kind;
+  int64_t d;
+  const int64_t* col_ptr;  /* device [n_store+1]                                    */
+  const int32_t* row_idx;  /* device [nnz]                                          */
+  const float* vals;       /* device [nnz]                                          */
+  const float* sq;
+  float* alpha;
+  const float* u;
+  const int32_t* seq;
+  const int64_t* work_prefix;
+  int32_t n_parts;
+  double a, lam, n_coords;
+  int32_t iid;
+  float* dv_work;
+  int32_t n_workers;
+  float* delta_v;
+  int32_t* status;
+} syscd_sparse_epoch_args;
+
+int syscd_sparse_epoch_workers(int64_t d, int32_t n_parts, int32_t* n_workers);
+int syscd_sparse_epoch(const syscd_sparse_epoch_args* e, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Reduction + epilogue (reduce_replicas solvers.py:112-125 at node/global
+ * level, solvers.py:393,423; then grad_f objective.py:105-110 for the next
+ * round, solvers.py:412).
+ *   dv[i]  = sum_{w < n_workers} partials[w*part_ld + i]   (ascending w)
+ *   if v:  v[i] += dv[i]  (fp64)  and  u[i] = grad f(v)[i]
+ * v == NULL: only dv is produced (the multi-GPU path all-reduces dv first).
+ * ------------------------------------------------------------------------ */
+int syscd_reduce_partials(const float* partials, int64_t part_ld, int32_t n_workers, int64_t d,
+                          float* dv, void* stream);
+int syscd_apply_dv(int32_t kind, int64_t d, const float* dv, double* v, const float* y,
+                   double lam, double n_coords, float* u, void* stream);
+/* u = grad f(v) + drift * (v_node - v)   (solvers.py:379-382 for T2 > 1) */
+int syscd_grad(int32_t kind, int64_t d, const double* v, const float* y, double lam,
+               double n_coords, const double* v_node, double drift, float* u, void* stream);
+/* fp64 certificate point for the duality gap: primal kinds w = grad f(v),
+ * dual kinds w = v / (lam n). */
+int syscd_dual_point(int32_t kind, int64_t d, const double* v, const float* y, double lam,
+                     double n_coords, double* w, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Metrics (fresh shared vector, fp64 accumulation): full_objective
+ * (objective.py:95-102) = matvec (dataset.py:100-110) + loss/penalty values;
+ * rmatvec (dataset.py:112-116) for the duality gap; column norms
+ * (compute_stats dataset.py:307).
+ * ------------------------------------------------------------------------ */
+int syscd_dense_matvec(int64_t d, int64_t n, int64_t lda, const float* A, const float* x,
+                       double* out, double* work, int64_t work_bytes, void* stream);
+int syscd_dense_rmatvec(int64_t d, int64_t n, int64_t lda, const float* A, const double* w,
+                        double* out, void* stream);
+int syscd_dense_col_sq_norms(int64_t d, int64_t n, int64_t lda, const float* A, float* out,
+                             void* stream);
+int syscd_sparse_matvec(int64_t d, int64_t n, const int64_t* col_ptr, const int32_t* row_idx,
+                        const float* vals, const float* x, double* out, void* stream);
+int syscd_sparse_rmatvec(int64_t n, const int64_t* col_ptr, const int32_t* row_idx,
+                         const float* vals, const double* w, double* out, void* stream);
+int syscd_sparse_col_sq_norms(int64_t n, const int64_t* col_ptr, const float* vals, float* out,
+                              void* stream);
+
+/* Objective / gap terms (fp64).  out[0..7] (see paper_1911_07722_b200/metrics.py):
+ *   mode 0: out[0] = f(v), out[1] = sum_j g(alpha_j)
+ *   mode 1: dual-certificate terms for the gap given atw = A^T w.      */
+int syscd_objective_terms(int32_t kind, int64_t d, int64_t n, const double* v, const float* y,
+                          const float* alpha, double lam, double n_coords, double* out,
+                          double* work, void* stream);
+int syscd_gap_terms(int32_t kind, int64_t d, int64_t n, const double* v, const float* y,
+                    const double* atw, double lam, double n_coords, double scale, double* out,
+                    double* work, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SYSCD_B200_H_ */

@@ -1,0 +1,211 @@
+// Shared device helpers: status codes, objective kinds, per-coordinate steps,
+// and the sm_100a PTX wrappers (mbarrier, 1-D bulk TMA, DSMEM st.async).
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "../../include/syscd_b200.h"
+
+namespace syscd {
+
+// ---------------------------------------------------------------------------
+// per-coordinate step: argmin_delta lin*delta + (a q/2) delta^2 + g_j(alpha+delta)
+// Ridge/primal-logistic row = reference surrogate_delta (objective.py:213-215);
+// the others are SURVEY Appendix A.  Computed in fp64 on every thread of the
+// worker (uniform), returns the new coordinate value.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double sigmoid_d(double s) {
+  if (s >= 0.0) return 1.0 / (1.0 + exp(-s));
+  double e = exp(s);
+  return e / (1.0 + e);
+}
+
+// Root of h(s) = lin + aq (sigma(s) - alpha) + s/n in log-odds s (the oracle's
+// logistic_dual_newton, oracle/objectives.py): bracketed Newton + bisection.
+__device__ __forceinline__ double logistic_dual_solve(double lin, double aq, double alpha,
+                                                      double n) {
+  const double inv_n = 1.0 / n;
+  double lo = -n * (lin + aq * (1.0 - alpha)) - 1.0;
+  double hi = n * (aq * alpha - lin) + 1.0;
+  double s;
+  if (alpha > 0.0 && alpha < 1.0) {
+    s = log(alpha) - log1p(-alpha);
+  } else {
+    s = 0.0;
+  }
+  s = fmin(fmax(s, lo), hi);
+  for (int it = 0; it < 100; ++it) {
+    double t = sigmoid_d(s);
+    double h = lin + aq * (t - alpha) + s * inv_n;
+    if (h > 0.0) {
+      hi = s;
+    } else if (h < 0.0) {
+      lo = s;
+    } else {
+      break;
+    }
+    double dh = aq * t * (1.0 - t) + inv_n;
+    double ns = s - h / dh;
+    if (!(lo < ns && ns < hi)) ns = 0.5 * (lo + hi);
+    double step = ns - s;
+    s = ns;
+    if (fabs(step) <= 1e-13 * fmax(1.0, fabs(s))) break;
+  }
+  return sigmoid_d(s);
+}
+
+__device__ __forceinline__ double coord_step(int kind, double lin, double a, double q, double lam,
+                                             double alpha, double n) {
+  switch (kind) {
+    case SYSCD_RIDGE:
+    case SYSCD_LOGISTIC:
+      return alpha - (lin + lam * alpha) / (a * q + lam);
+    case SYSCD_LASSO: {
+      double aq = a * q;
+      if (aq <= 0.0) return 0.0;
+      double z = alpha - lin / aq;
+      double m = fabs(z) - lam / aq;
+      return m > 0.0 ? copysign(m, z) : 0.0;
+    }
+    case SYSCD_SVM_DUAL: {
+      double aq = a * q;
+      if (aq <= 0.0) return 1.0;
+      double z = alpha - (lin - 1.0 / n) / aq;
+      return fmin(fmax(z, 0.0), 1.0);
+    }
+    default:  // SYSCD_LOGISTIC_DUAL
+      return logistic_dual_solve(lin, a * q, alpha, n);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// PTX wrappers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAITC_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// 1-D bulk copy global -> this CTA's shared memory, completion on `bar`.
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t cluster_map(uint32_t local_smem_addr, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(local_smem_addr), "r"(rank));
+  return out;
+}
+
+// Remote 4-byte store into a peer CTA's shared memory, signalling the peer's
+// mbarrier with complete_tx(4).
+__device__ __forceinline__ void st_async_f32(uint32_t remote_addr, float v, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(
+                   remote_addr),
+               "r"(__float_as_uint(v)), "r"(remote_bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace syscd
+
+#define SYSCD_CUDA_TRY(expr)                                   \
+  do {                                                         \
+    cudaError_t _e = (expr);                                   \
+    if (_e != cudaSuccess) {                                   \
+      syscd::set_error("%s: %s", #expr, cudaGetErrorString(_e)); \
+      return SYSCD_ECUDA;                                      \
+    }                                                          \
+  } while (0)
+
+namespace syscd {
+void set_error(const char* fmt, ...);
+}

@@ -1,0 +1,513 @@
+// Dense SySCD round on sm_100a.
+//
+// Reference semantics (pkg/src/syscd/solvers.py:289-334, 384-393): every
+// partition p walks its coordinate sequence j_1..j_m; per coordinate
+//     lin   = x_j . u + a x_j . dv          (u = lin_vec, dv = private replica)
+//     alpha_j <- step(lin, a, q_j, lam, alpha_j)
+//     dv   += delta x_j
+// and the node replica becomes v + sum_p dv_p.
+//
+// B200 mapping (DESIGN.md section "dense epoch kernel"):
+//  * a partition runs on one thread-block cluster of C CTAs; CTA `rank` owns
+//    rows [rank*CTA_ROWS, (rank+1)*CTA_ROWS) of the shared vector;
+//  * the replica lives in registers as w = u + a dv (one fp32 per owned row,
+//    so lin = x_j . w and the axpy is w += a delta x_j); at the end of a
+//    partition the cluster folds (w - u)/a into its slice of `partials`;
+//  * one producer warp per CTA streams the CTA's slice of each column into a
+//    ring of shared-memory stages with 1-D bulk TMA (cp.async.bulk +
+//    mbarrier complete_tx), running ahead of the consumers by the ring depth;
+//    the column sequence is known from the plan, so prefetch crosses bucket
+//    and partition boundaries;
+//  * consumer warps read each staged chunk twice (dot, then axpy) from smem,
+//    reduce the dot warp -> CTA (named barrier) -> cluster (st.async of one
+//    float into every peer's smem, completing the peer's mbarrier); every CTA
+//    then sums the C partials in rank order, so lin is bit-identical across
+//    the cluster and the step is computed redundantly in fp64;
+//  * clusters process disjoint contiguous ranges of partitions (balanced by
+//    update count) and accumulate their partitions' replicas into one
+//    partials row each, in a fixed order: the result is deterministic.
+#include <algorithm>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace syscd {
+
+struct DenseArgs {
+  const float* A;
+  int64_t lda;
+  int64_t d;
+  const float* sq;
+  float* alpha;
+  const float* u;
+  const int32_t* seq;
+  const int64_t* wp;
+  int32_t n_parts;
+  float a;
+  double a_d;
+  double lam;
+  double n_coords;
+  int32_t kind;
+  int32_t iid;
+  int32_t stages;
+  int32_t cluster;
+  int32_t evict_first;
+  float* partials;
+  int64_t part_ld;
+  int32_t* status;
+};
+
+constexpr int kMetaRing = 64;
+constexpr int kMaxCluster = 16;
+
+template <int NTC, int RC, int NCH>
+struct DenseCfg {
+  static constexpr int kNTC = NTC;
+  static constexpr int kNWC = NTC / 32;
+  static constexpr int kRC = RC;
+  static constexpr int kNCH = NCH;
+  static constexpr int kR = RC * NCH;
+  static constexpr int kChunkRows = NTC * RC;
+  static constexpr int kCtaRows = kChunkRows * NCH;
+  static constexpr int kThreads = NTC + 32;
+};
+
+struct SmemLayout {
+  size_t ring, full, empty, xbar, slots, red, meta, range, total;
+};
+
+__host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+__host__ __device__ inline SmemLayout smem_layout(int stages, int chunk_rows) {
+  SmemLayout L;
+  L.ring = 0;
+  size_t o = align_up((size_t)stages * chunk_rows * 4, 128);
+  L.full = o;
+  o += (size_t)stages * 8;
+  L.empty = o;
+  o += (size_t)stages * 8;
+  L.xbar = o;
+  o += 2 * 8;
+  L.slots = o;
+  o += 2 * kMaxCluster * 4;
+  L.red = o;
+  o += 2 * 32 * 4;
+  L.meta = o;
+  o += kMetaRing * 4;
+  L.range = o;
+  o += 4 * 8;
+  L.total = align_up(o, 128);
+  return L;
+}
+
+__device__ __forceinline__ int64_t lower_bound_i64(const int64_t* a, int n, int64_t key) {
+  int lo = 0, hi = n;  // first index in [0, n) with a[idx] >= key, or n
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (a[mid] < key) {
+      lo = mid + 1;
+    } else {
+      hi = mid;
+    }
+  }
+  return lo;
+}
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args) {
+  constexpr int NTC = Cfg::kNTC;
+  constexpr int NWC = Cfg::kNWC;
+  constexpr int RC = Cfg::kRC;
+  constexpr int NCH = Cfg::kNCH;
+  constexpr int R = Cfg::kR;
+  constexpr int CHUNK = Cfg::kChunkRows;
+  constexpr int CTA_ROWS = Cfg::kCtaRows;
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int S = args.stages;
+  const SmemLayout L = smem_layout(S, CHUNK);
+  float* ring = reinterpret_cast<float*>(smem + L.ring);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.full);
+  uint64_t* empty = reinterpret_cast<uint64_t*>(smem + L.empty);
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(smem + L.xbar);
+  float* slots = reinterpret_cast<float*>(smem + L.slots);
+  float* red = reinterpret_cast<float*>(smem + L.red);
+  int* meta = reinterpret_cast<int*>(smem + L.meta);
+  int64_t* range = reinterpret_cast<int64_t*>(smem + L.range);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+  const int C = args.cluster;
+  const uint32_t rank = cluster_rank();
+  const int g = blockIdx.x / C;
+  const int G = gridDim.x / C;
+  const int64_t row0 = (int64_t)rank * CTA_ROWS;
+  const int64_t d = args.d;
+
+  for (int i = tid; i < S * CHUNK; i += blockDim.x) ring[i] = 0.f;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NWC);
+    }
+    mbar_init(&xbar[0], 1);
+    mbar_init(&xbar[1], 1);
+    const int64_t total = args.wp[args.n_parts];
+    const int64_t t_lo = (int64_t)((__int128)total * g / G);
+    const int64_t t_hi = (int64_t)((__int128)total * (g + 1) / G);
+    int64_t p_lo = g == 0 ? 0 : lower_bound_i64(args.wp, args.n_parts + 1, t_lo);
+    int64_t p_hi = g == G - 1 ? args.n_parts : lower_bound_i64(args.wp, args.n_parts + 1, t_hi);
+    if (p_lo > args.n_parts) p_lo = args.n_parts;
+    if (p_hi > args.n_parts) p_hi = args.n_parts;
+    range[0] = p_lo;
+    range[1] = p_hi;
+    fence_mbar_init();
+    fence_proxy_async();
+  }
+  __syncthreads();
+  cluster_sync_all();
+
+  const int64_t p_lo = range[0];
+  const int64_t p_hi = range[1];
+  const int64_t s_begin = args.wp[p_lo];
+  const int64_t s_end = args.wp[p_hi];
+
+  if (warp == NWC) {
+    // ------------------------------------------------------------ producer
+    const uint64_t policy = args.evict_first ? policy_evict_first() : policy_evict_last();
+    uint32_t cc = 0;
+    int jreg = 0;
+    for (int64_t s = s_begin; s < s_end; ++s) {
+      const int64_t rel = s - s_begin;
+      if ((rel & 31) == 0) {
+        const int64_t q = s + lane;
+        jreg = q < s_end ? args.seq[q] : 0;
+      }
+      const int j = __shfl_sync(0xffffffffu, jreg, (int)(rel & 31));
+      if (lane == 0) {
+        const float* col = args.A + (int64_t)j * args.lda;
+#pragma unroll 1
+        for (int c = 0; c < NCH; ++c, ++cc) {
+          const uint32_t stage = cc % (uint32_t)S;
+          const uint32_t use = cc / (uint32_t)S;
+          mbar_wait(&empty[stage], (use & 1u) ^ 1u);
+          if (c == 0) meta[s & (kMetaRing - 1)] = j;
+          const int64_t r0 = row0 + (int64_t)c * CHUNK;
+          int64_t valid = d - r0;
+          valid = valid < 0 ? 0 : (valid > CHUNK ? CHUNK : valid);
+          const uint32_t bytes = (uint32_t)(((valid + 3) / 4) * 16);
+          if (bytes) {
+            mbar_arrive_expect_tx(&full[stage], bytes);
+            tma_load_1d(ring + (size_t)stage * CHUNK, col + r0, bytes, &full[stage], policy);
+          } else {
+            mbar_arrive(&full[stage]);
+          }
+        }
+      }
+      __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------------------ consumers
+    // owned row of register slot q = c*RC + k is row0 + q*NTC + tid; slots
+    // q >= qmax lie past d and stay zero (their staged values are ignored).
+    const int64_t rem = d - row0 - tid;
+    const int qmax = rem <= 0 ? 0 : (int)min((int64_t)R, (rem + NTC - 1) / NTC);
+    const float* ub = args.u + row0 + tid;
+    float w[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) w[q] = q < qmax ? ub[q * NTC] : 0.f;
+    const float a = args.a;
+    const float inv_a = (float)(1.0 / args.a_d);
+    float* out = args.partials + (int64_t)g * args.part_ld + row0 + tid;
+    bool flushed = false;
+    int64_t part = p_lo;
+    while (part < p_hi && args.wp[part + 1] <= s_begin) ++part;
+    int64_t part_end = part < p_hi ? args.wp[part + 1] : s_end;
+    uint32_t cc = 0;
+    // exchange addresses: slot[buf][rank] and xbar[buf] in peer `lane`
+    uint32_t peer_slot = 0, peer_bar = 0;
+    if (warp == 0 && lane < C) {
+      peer_slot = cluster_map(smem_addr(slots + rank), (uint32_t)lane);
+      peer_bar = cluster_map(smem_addr(&xbar[0]), (uint32_t)lane);
+    }
+    for (int64_t s = s_begin; s < s_end; ++s) {
+      const uint32_t t = (uint32_t)(s - s_begin);
+      const uint32_t buf = t & 1u;
+      float acc = 0.f;
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        const uint32_t stage = (cc + c) % (uint32_t)S;
+        const uint32_t use = (cc + c) / (uint32_t)S;
+        mbar_wait(&full[stage], use & 1u);
+        const float* x = ring + (size_t)stage * CHUNK + tid;
+#pragma unroll
+        for (int k = 0; k < RC; ++k) acc = fmaf(x[k * NTC], w[c * RC + k], acc);
+      }
+      const int j = meta[s & (kMetaRing - 1)];
+      float aj = 0.f;
+      if (!args.iid) aj = args.alpha[j];
+      const float qj = args.sq[j];
+      acc = warp_sum(acc);
+      if (lane == 0) red[buf * 32 + warp] = acc;
+      named_bar_sync(1, NTC);
+      if (warp == 0) {
+        float v = lane < NWC ? red[buf * 32 + lane] : 0.f;
+        v = warp_sum(v);
+        if (lane < C) st_async_f32(peer_slot + buf * kMaxCluster * 4, v, peer_bar + buf * 8);
+        if (lane == 0) mbar_arrive_expect_tx(&xbar[buf], 4u * (uint32_t)C);
+      }
+      mbar_wait_cluster(&xbar[buf], (t >> 1) & 1u);
+      float lin = 0.f;
+      for (int r = 0; r < C; ++r) lin += slots[buf * kMaxCluster + r];
+      if (args.iid) aj = *(volatile float*)(args.alpha + j);
+      const double anew = coord_step(args.kind, (double)lin, args.a_d, (double)qj, args.lam,
+                                     (double)aj, args.n_coords);
+      float delta;
+      if (isfinite(anew)) {
+        const float an = (float)anew;
+        delta = an - aj;
+        if (rank == 0 && tid == 0) args.alpha[j] = an;
+      } else {
+        delta = 0.f;
+        if (rank == 0 && tid == 0) atomicOr(args.status, SYSCD_ENONFINITE);
+      }
+      const float sd = a * delta;
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        const uint32_t stage = (cc + c) % (uint32_t)S;
+        const float* x = ring + (size_t)stage * CHUNK + tid;
+#pragma unroll
+        for (int k = 0; k < RC; ++k) {
+          const int q = c * RC + k;
+          if (q < qmax) w[q] = fmaf(sd, x[k * NTC], w[q]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+      }
+      cc += NCH;
+      if (s + 1 == part_end) {
+        // fold this partition's replica (w - u)/a into the cluster's partial sum
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          if (q < qmax) {
+            const float uu = ub[q * NTC];
+            const float dv = (w[q] - uu) * inv_a;
+            out[q * NTC] = flushed ? out[q * NTC] + dv : dv;
+            w[q] = uu;
+          }
+        }
+        flushed = true;
+        ++part;
+        while (part < p_hi && args.wp[part + 1] <= s + 1) ++part;
+        part_end = part < p_hi ? args.wp[part + 1] : s_end;
+      }
+    }
+    if (!flushed) {
+#pragma unroll
+      for (int q = 0; q < R; ++q)
+        if (q < qmax) out[q * NTC] = 0.f;
+    }
+  }
+  __syncwarp();
+  cluster_sync_all();
+}
+
+// ---------------------------------------------------------------------------
+// host side: configuration table and launch
+// ---------------------------------------------------------------------------
+struct KernelEntry {
+  int ntc, rc, nch;
+  const void* fn;
+  int threads;
+  int max_clusters[kMaxCluster + 1];  // per cluster size, 0 = unknown, -1 = not launchable
+};
+
+template <int NTC, int RC, int NCH>
+static KernelEntry make_entry() {
+  KernelEntry e;
+  e.ntc = NTC;
+  e.rc = RC;
+  e.nch = NCH;
+  e.fn = (const void*)&k_dense_epoch<DenseCfg<NTC, RC, NCH>>;
+  e.threads = NTC + 32;
+  for (int i = 0; i <= kMaxCluster; ++i) e.max_clusters[i] = 0;
+  return e;
+}
+
+// (consumer threads, rows per thread per chunk, chunks per column slice);
+// consumer warps + 1 producer warp is a power of two so the register file is
+// split without rounding loss (<= 128 regs/thread at 16 warps).
+static KernelEntry g_table[] = {
+    make_entry<32, 1, 1>(),  make_entry<96, 1, 1>(),  make_entry<224, 2, 1>(),
+    make_entry<224, 4, 1>(), make_entry<480, 4, 1>(), make_entry<480, 4, 2>(),
+    make_entry<480, 4, 4>(), make_entry<480, 8, 4>(), make_entry<480, 9, 6>(),
+};
+static std::mutex g_table_mu;
+constexpr int kTableSize = sizeof(g_table) / sizeof(g_table[0]);
+
+static int entry_rows(const KernelEntry& e) { return e.ntc * e.rc * e.nch; }
+
+static int choose_stages(const KernelEntry& e, size_t smem_budget) {
+  const size_t stage_bytes = (size_t)e.ntc * e.rc * 4;
+  const size_t fixed = smem_layout(0, e.ntc * e.rc).total + 1024;
+  int s = (int)((smem_budget - fixed) / (stage_bytes + 16));
+  s = std::min(s, 32);
+  s = s / e.nch * e.nch;
+  return s;
+}
+
+static int query_max_clusters(KernelEntry& e, int C, int stages, size_t smem) {
+  if (e.max_clusters[C] != 0) return e.max_clusters[C];
+  cudaFuncSetAttribute(e.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (C > 8) cudaFuncSetAttribute(e.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C, 1, 1);
+  cfg.blockDim = dim3(e.threads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  cudaError_t err = cudaOccupancyMaxActiveClusters(&n, e.fn, &cfg);
+  if (err != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = -1;
+  }
+  e.max_clusters[C] = n;
+  (void)stages;
+  return n;
+}
+
+struct Choice {
+  int idx;
+  int C;
+  int G;
+  int stages;
+  size_t smem;
+};
+
+static int choose(int64_t d, int32_t n_parts, Choice* out) {
+  std::lock_guard<std::mutex> lock(g_table_mu);
+  int dev = 0;
+  SYSCD_CUDA_TRY(cudaGetDevice(&dev));
+  int sms = 0, smem_optin = 0;
+  SYSCD_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  SYSCD_CUDA_TRY(
+      cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const size_t budget = (size_t)std::min(smem_optin, 200 * 1024);
+  double best = 1e300;
+  Choice bc = {-1, 0, 0, 0, 0};
+  for (int i = 0; i < kTableSize; ++i) {
+    KernelEntry& e = g_table[i];
+    const int rows = entry_rows(e);
+    const int C = (int)((d + rows - 1) / rows);
+    if (C < 1 || C > kMaxCluster) continue;
+    const int stages = choose_stages(e, budget);
+    if (stages < 2 * e.nch) continue;
+    const size_t smem = smem_layout(stages, e.ntc * e.rc).total;
+    const int maxc = query_max_clusters(e, C, stages, smem);
+    if (maxc <= 0) continue;
+    const int G = std::max(1, std::min(maxc, (int)n_parts));
+    // per-step cycles: staged reads (dot + axpy) + reduction latency, against
+    // the HBM share of the G*C SMs streaming this geometry
+    const double lds = (double)rows * 8.0 / 128.0;
+    const double sync = 700.0 + 25.0 * C;
+    const double hbm = (double)rows * 4.0 / (6.5e12 / (double)(G * C)) * 1.9e9;
+    const double t = std::max(lds + sync, hbm) / (double)G;
+    if (t < best * 0.999) {
+      best = t;
+      bc = {i, C, G, stages, smem};
+    }
+  }
+  if (bc.idx < 0) {
+    set_error("no dense epoch configuration covers d=%lld (max %d rows per cluster)",
+              (long long)d, 16 * 25920);
+    return SYSCD_EINVAL;
+  }
+  *out = bc;
+  return SYSCD_OK;
+}
+
+}  // namespace syscd
+
+using namespace syscd;
+
+extern "C" int syscd_dense_epoch_workers(int64_t d, int32_t n_parts, int32_t* n_workers,
+                                         int32_t* cluster) {
+  if (d < 1 || n_parts < 1 || !n_workers) {
+    set_error("syscd_dense_epoch_workers: invalid arguments");
+    return SYSCD_EINVAL;
+  }
+  Choice ch;
+  int st = choose(d, n_parts, &ch);
+  if (st) return st;
+  *n_workers = ch.G;
+  if (cluster) *cluster = ch.C;
+  return SYSCD_OK;
+}
+
+extern "C" int syscd_dense_epoch(const syscd_dense_epoch_args* e, void* stream) {
+  if (!e || !e->A || !e->sq || !e->alpha || !e->u || !e->seq || !e->work_prefix ||
+      !e->partials || !e->status || e->d < 1 || e->n_parts < 1 || e->lda < e->d ||
+      (e->lda % 4) != 0 || !(e->a > 0.0) || !(e->lam > 0.0)) {
+    set_error("syscd_dense_epoch: invalid arguments");
+    return SYSCD_EINVAL;
+  }
+  if ((((uintptr_t)e->A) & 15) != 0) {
+    set_error("syscd_dense_epoch: A must be 16-byte aligned");
+    return SYSCD_EINVAL;
+  }
+  Choice ch;
+  int st = choose(e->d, e->n_parts, &ch);
+  if (st) return st;
+  if (e->part_ld < e->d) {
+    set_error("syscd_dense_epoch: part_ld < d");
+    return SYSCD_EINVAL;
+  }
+  const KernelEntry& ke = g_table[ch.idx];
+  DenseArgs args;
+  args.A = e->A;
+  args.lda = e->lda;
+  args.d = e->d;
+  args.sq = e->sq;
+  args.alpha = e->alpha;
+  args.u = e->u;
+  args.seq = e->seq;
+  args.wp = e->work_prefix;
+  args.n_parts = e->n_parts;
+  args.a = (float)e->a;
+  args.a_d = e->a;
+  args.lam = e->lam;
+  args.n_coords = e->n_coords;
+  args.kind = e->kind;
+  args.iid = e->iid;
+  args.stages = ch.stages;
+  args.cluster = ch.C;
+  // keep a matrix that fits comfortably in the 126 MB L2 resident across
+  // rounds; stream larger ones with evict_first so they do not flush u/alpha
+  args.evict_first = ((double)e->lda * 4.0 * (double)e->n_store) > 64.0 * 1024 * 1024 ? 1 : 0;
+  args.partials = e->partials;
+  args.part_ld = e->part_ld;
+  args.status = e->status;
+
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ch.G * ch.C, 1, 1);
+  cfg.blockDim = dim3(ke.threads, 1, 1);
+  cfg.dynamicSmemBytes = ch.smem;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = ch.C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void* params[] = {&args};
+  SYSCD_CUDA_TRY(cudaLaunchKernelExC(&cfg, ke.fn, params));
+  return SYSCD_OK;
+}

@@ -1,0 +1,239 @@
+"""Column-major training data (mirror of pkg/src/syscd/dataset.py).
+
+ColumnMatrix keeps the reference's constructor and accessors
+(dataset.py:24-130) but stores float32, the compute type of the GPU path, and
+can also wrap data that already lives on the GPU (``ColumnMatrix.from_device``)
+so that the 3.2 GB / 32 GB configurations never round-trip through the host.
+
+Device layout: a dense matrix is a
+(n_cols, lda) float32 torch tensor, i.e. column-major A with leading dimension
+lda = d rounded up to a multiple of 4 (16-byte rows for the bulk TMA copies,
+padding zero-filled).  A sparse matrix is CSC: int64 col_ptr, int32 row_idx,
+float32 values.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+COORDINATES_ARE_FEATURES = "coordinates_are_features"
+COORDINATES_ARE_EXAMPLES = "coordinates_are_examples"
+
+
+def padded_ld(d):
+    return (int(d) + 3) // 4 * 4
+
+
+class ColumnMatrix:
+    """Training data stored column by column (dense or per-column sparse)."""
+
+    def __init__(self, n_rows, n_cols, dense=None, sparse_cols=None, csc=None):
+        given = sum(x is not None for x in (dense, sparse_cols, csc))
+        if given != 1:
+            raise ValueError("exactly one of dense / sparse_cols must be given")
+        self.n_rows = int(n_rows)
+        self.n_cols = int(n_cols)
+        self._dev_dense = None
+        self._dev_csc = None
+        if dense is not None:
+            dense = np.asfortranarray(dense, dtype=np.float32)
+            if dense.shape != (self.n_rows, self.n_cols):
+                raise ValueError("dense array shape does not match dims")
+            if not np.all(np.isfinite(dense)):
+                raise ValueError("non-finite entries in data matrix")
+            self.storage_kind = "dense"
+            self._dense = dense
+            self._csc = None
+        else:
+            if sparse_cols is not None:
+                if len(sparse_cols) != self.n_cols:
+                    raise ValueError("sparse column count does not match n_cols")
+                ptr = np.zeros(self.n_cols + 1, dtype=np.int64)
+                idx_l, val_l = [], []
+                for j, (idx, vals) in enumerate(sparse_cols):
+                    idx = np.asarray(idx, dtype=np.int64)
+                    vals = np.asarray(vals, dtype=np.float64)
+                    if idx.shape != vals.shape:
+                        raise ValueError(f"column {j}: index/value length mismatch")
+                    idx_l.append(idx)
+                    val_l.append(vals)
+                    ptr[j + 1] = ptr[j] + idx.size
+                indices = np.concatenate(idx_l) if idx_l else np.zeros(0, np.int64)
+                values = np.concatenate(val_l) if val_l else np.zeros(0)
+            else:
+                ptr, indices, values = (np.asarray(csc[0], dtype=np.int64),
+                                        np.asarray(csc[1], dtype=np.int64),
+                                        np.asarray(csc[2], dtype=np.float64))
+                if ptr.shape != (self.n_cols + 1,) or ptr[0] != 0 or ptr[-1] != indices.size:
+                    raise ValueError("bad CSC column pointer")
+            self._check_sparse(ptr, indices, values)
+            self.storage_kind = "sparse"
+            self._dense = None
+            self._csc = (ptr, indices.astype(np.int32), values.astype(np.float32))
+
+    def _check_sparse(self, ptr, indices, values):
+        if indices.shape != values.shape:
+            raise ValueError("index/value length mismatch")
+        if np.any(np.diff(ptr) < 0):
+            raise ValueError("column pointer not monotone")
+        if indices.size:
+            if indices.min() < 0 or indices.max() >= self.n_rows:
+                raise ValueError("row index out of range")
+            d = np.diff(indices)
+            starts = ptr[1:-1]
+            ok = np.ones(d.size, dtype=bool)
+            ok[starts[(starts > 0) & (starts < indices.size)] - 1] = False
+            if np.any((d <= 0) & ok):
+                raise ValueError("indices not strictly increasing within a column")
+        if not np.all(np.isfinite(values)):
+            raise ValueError("non-finite values")
+
+    # -- device-resident construction ---------------------------------------
+    @classmethod
+    def from_device(cls, At, n_rows):
+        """Wrap a (n_cols, lda) float32 CUDA tensor holding A column-major."""
+        import torch
+        if At.dtype != torch.float32 or not At.is_cuda or At.dim() != 2 or not At.is_contiguous():
+            raise ValueError("from_device expects a contiguous float32 CUDA tensor (n_cols, lda)")
+        if At.shape[1] % 4 != 0 or At.shape[1] < n_rows:
+            raise ValueError("lda must be >= n_rows and a multiple of 4")
+        obj = cls.__new__(cls)
+        obj.n_rows = int(n_rows)
+        obj.n_cols = int(At.shape[0])
+        obj.storage_kind = "dense"
+        obj._dense = None
+        obj._csc = None
+        obj._dev_dense = At
+        obj._dev_csc = None
+        return obj
+
+    @classmethod
+    def from_device_csc(cls, col_ptr, row_idx, vals, n_rows):
+        """Wrap CUDA CSC tensors (int64 col_ptr, int32 row_idx, float32 vals)."""
+        obj = cls.__new__(cls)
+        obj.n_rows = int(n_rows)
+        obj.n_cols = int(col_ptr.shape[0] - 1)
+        obj.storage_kind = "sparse"
+        obj._dense = None
+        obj._csc = None
+        obj._dev_dense = None
+        obj._dev_csc = (col_ptr, row_idx, vals)
+        return obj
+
+    # -- reference accessors (host) ------------------------------------------
+    def _host_dense(self):
+        if self._dense is None and self._dev_dense is not None:
+            self._dense = np.asfortranarray(
+                self._dev_dense[:, : self.n_rows].cpu().numpy().T)
+        return self._dense
+
+    def _host_csc(self):
+        if self._csc is None and self._dev_csc is not None:
+            cp, ri, va = (t.cpu().numpy() for t in self._dev_csc)
+            self._csc = (cp.astype(np.int64), ri.astype(np.int32), va.astype(np.float32))
+        return self._csc
+
+    def column(self, j):
+        if self.storage_kind == "dense":
+            return self._host_dense()[:, j]
+        ptr, idx, val = self._host_csc()
+        return idx[ptr[j]:ptr[j + 1]].astype(np.intp), val[ptr[j]:ptr[j + 1]].astype(np.float64)
+
+    def to_dense(self):
+        if self.storage_kind == "dense":
+            return self._host_dense().astype(np.float64)
+        out = np.zeros((self.n_rows, self.n_cols), order="F")
+        ptr, idx, val = self._host_csc()
+        for j in range(self.n_cols):
+            out[idx[ptr[j]:ptr[j + 1]], j] = val[ptr[j]:ptr[j + 1]]
+        return out
+
+    def csc(self):
+        """(col_ptr int64, row_idx int32, values float32) host arrays."""
+        if self.storage_kind != "sparse":
+            raise ValueError("not a sparse matrix")
+        return self._host_csc()
+
+    def nnz(self):
+        if self.storage_kind == "dense":
+            if self._dense is not None:
+                return int(np.count_nonzero(self._dense))
+            return int((self._dev_dense[:, : self.n_rows] != 0).sum().item())
+        if self._csc is not None:
+            return int(self._csc[0][-1])
+        return int(self._dev_csc[0][-1].item())
+
+
+@dataclass
+class LabeledDataset:
+    """A ColumnMatrix plus labels: one per shared-vector row in the feature
+    orientation, one per column in the example (dual) orientation
+    (dataset.py:132-157)."""
+
+    matrix: ColumnMatrix
+    labels: np.ndarray
+    orientation: str = COORDINATES_ARE_FEATURES
+
+    def __post_init__(self):
+        if self.orientation not in (COORDINATES_ARE_FEATURES, COORDINATES_ARE_EXAMPLES):
+            raise ValueError(f"unknown orientation: {self.orientation}")
+        self.labels = np.ascontiguousarray(self.labels, dtype=np.float64)
+        expected = (self.matrix.n_rows if self.orientation == COORDINATES_ARE_FEATURES
+                    else self.matrix.n_cols)
+        if self.labels.shape != (expected,):
+            raise ValueError("label count does not match dataset orientation")
+        if not np.all(np.isfinite(self.labels)):
+            raise ValueError("non-finite labels")
+
+
+@dataclass
+class DatasetStats:
+    """Per-column squared norms plus the spectral constant (dataset.py:160-166)."""
+
+    column_sq_norms: np.ndarray
+    c_A: float
+    max_col_sq_norm: float
+
+
+def compute_stats(matrix, with_spectral=False, power_iters=200, tol=1e-9):
+    """Column squared norms on the GPU (dataset.py:307).  c_A (the power
+    iteration of dataset.py:308-321) is theory-only; it runs on the GPU when
+    requested, else c_A is NaN."""
+    from .device import column_sq_norms, spectral_constant
+    sq = column_sq_norms(matrix)
+    c_a = spectral_constant(matrix, power_iters, tol) if with_spectral else float("nan")
+    return DatasetStats(column_sq_norms=sq, c_A=c_a, max_col_sq_norm=float(sq.max()))
+
+
+# ---------------------------------------------------------------------------
+# reference-style synthetic generators (dataset.py:262-295), same streams
+# ---------------------------------------------------------------------------
+_SYNTH_DENSE, _SYNTH_SPARSE, _SYNTH_LABELS = 100, 101, 102
+
+
+def _rng(seed, tag):
+    return np.random.default_rng(np.random.SeedSequence(seed, spawn_key=(tag,)))
+
+
+def generate_synthetic_dense(n_examples, n_features, seed):
+    if n_examples < 1 or n_features < 1:
+        raise ValueError("n_examples and n_features must be >= 1")
+    data = np.asfortranarray(_rng(seed, _SYNTH_DENSE).random((n_examples, n_features)))
+    labels = _rng(seed, _SYNTH_LABELS).integers(0, 2, size=n_examples) * 2.0 - 1.0
+    return LabeledDataset(ColumnMatrix(n_examples, n_features, dense=data), labels)
+
+
+def generate_synthetic_sparse(n_examples, n_features, density, seed):
+    if n_examples < 1 or n_features < 1:
+        raise ValueError("n_examples and n_features must be >= 1")
+    if not (0.0 < density <= 1.0):
+        raise ValueError("density must be in (0, 1]")
+    g = _rng(seed, _SYNTH_SPARSE)
+    cols = []
+    for _ in range(n_features):
+        idx = np.nonzero(g.random(n_examples) < density)[0]
+        cols.append((idx, g.random(idx.size)))
+    labels = _rng(seed, _SYNTH_LABELS).integers(0, 2, size=n_examples) * 2.0 - 1.0
+    return LabeledDataset(ColumnMatrix(n_examples, n_features, sparse_cols=cols), labels)

@@ -1,0 +1,480 @@
+"""SySCD solver entry points on the GPU (mirror of pkg/src/syscd/solvers.py).
+
+run_syscd(problem, cfg, f_star) keeps the reference's signature, parameter
+contract (SolverConfig, solvers.py:44-88), result types (EpochMetrics,
+TrainResult, solvers.py:91-109), error behaviour (ValueError on bad
+configurations, NonFiniteUpdateError on a non-finite step, divergence as a
+result flag) and per-round structure (solvers.py:400-443):
+
+  round t1:  plan (device RNG, partitioning.py)  ->  epoch kernel (all K*P
+             partitions, private replicas)  ->  replica reduction  ->
+             [multi-GPU: NCCL all-reduce of dv]  ->  v += dv, u = grad f(v)
+  metrics:   fresh A alpha on the GPU, fp64 (excluded from the epoch time,
+             as the reference's `elapsed` is taken before _metrics_row).
+
+Everything on the path runs in libsyscd_b200.so; there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._lib import DenseEpochArgs, PlanDesc, SparseEpochArgs, call, lib
+from .device import DeviceProblem, Dist, _ptr, _stream, _torch
+from .objective import LOGISTIC, NonFiniteUpdateError
+from .partitioning import (
+    DEFAULT_CACHE_LINE_BYTES,
+    NODE_PARTITION,
+    RngStream,
+    build_buckets,
+    default_bucket_size,
+    static_node_partition,
+)
+
+DIVERGENCE_FACTOR = 1e6
+
+
+@dataclass
+class SolverConfig:
+    algorithm: str = "syscd"
+    K: int = 1                      # node groups (GPUs x logical nodes per GPU)
+    P: int = 1                      # threads (partitions) per node group
+    bucket_size: int | None = None  # None: cache_line_bytes / 8
+    cache_line_bytes: int = DEFAULT_CACHE_LINE_BYTES
+    T1: int | None = None           # fixed outer round count; None: run to tolerance
+    T2: int = 1                     # node-local rounds per global round
+    T3: int | None = None           # buckets per thread per round; None: all assigned
+    T4: int | None = None           # updates per bucket; None: bucket length (perm) / B (iid)
+    sampling: str = "perm"
+    repartition: str = "dynamic"
+    seed: int = 0
+    max_epochs: int = 100
+    tolerance: float = 1e-5
+    verify: bool = False
+    record_alpha: bool = False
+    # extensions; defaults keep the reference's behaviour
+    compute_gap: bool = False       # add the duality gap to every metrics row
+    metrics_every: int = 1          # evaluate metrics every k rounds (and the last)
+    plan_batch: int = 8             # rounds planned per device planning launch
+
+    def __post_init__(self):
+        if self.algorithm not in ("sequential", "wild", "syscd"):
+            raise ValueError(f"unknown algorithm: {self.algorithm}")
+        if self.K < 1 or self.P < 1 or self.T2 < 1:
+            raise ValueError("K, P and T2 must be >= 1")
+        if self.T3 is not None and self.T3 < 1:
+            raise ValueError("T3 must be >= 1")
+        if self.T4 is not None and self.T4 < 1:
+            raise ValueError("T4 must be >= 1")
+        if self.sampling not in ("perm", "iid"):
+            raise ValueError(f"unknown sampling mode: {self.sampling}")
+        if self.repartition not in ("dynamic", "static"):
+            raise ValueError(f"unknown repartition mode: {self.repartition}")
+        if self.tolerance <= 0.0:
+            raise ValueError("tolerance must be > 0")
+        if self.max_epochs < 0:
+            raise ValueError("max_epochs must be >= 0")
+        if self.metrics_every < 1 or self.plan_batch < 1:
+            raise ValueError("metrics_every and plan_batch must be >= 1")
+
+    def resolved_bucket_size(self):
+        if self.bucket_size is not None:
+            return self.bucket_size
+        return default_bucket_size(self.cache_line_bytes)
+
+    @property
+    def n_rounds(self):
+        return self.T1 if self.T1 is not None else self.max_epochs
+
+
+@dataclass
+class EpochMetrics:
+    epoch: int
+    objective: float
+    suboptimality: float | None
+    seconds: float
+    updates: int
+    rel_change: float
+    gap: float | None = None
+
+
+@dataclass
+class TrainResult:
+    alpha: np.ndarray
+    metrics: list
+    converged: bool
+    total_updates: int
+    diverged: bool = False
+    reason: str | None = None
+    alpha_snapshots: list = field(default_factory=list)
+
+
+def reduce_replicas(base, replicas):
+    """base + sum_r (replica_r - base), ascending r (solvers.py:112-125).
+
+    Host helper kept for API parity; the solver reduces device replicas with
+    syscd_reduce_partials in the same ascending order."""
+    base = np.asarray(base, dtype=np.float64)
+    if not replicas:
+        raise ValueError("need at least one replica")
+    for r in replicas:
+        if np.shape(r) != base.shape:
+            raise ValueError("replica length mismatch")
+    if len(replicas) == 1:
+        return np.array(replicas[0], dtype=np.float64)
+    acc = np.zeros_like(base)
+    for r in replicas:
+        acc += np.asarray(r, dtype=np.float64) - base
+    return base + acc
+
+
+# ---------------------------------------------------------------------------
+# GPU engine
+# ---------------------------------------------------------------------------
+class _Engine:
+    """Buffers and launches for one problem shard and one configuration."""
+
+    def __init__(self, problem, cfg, dist):
+        torch = _torch()
+        self.torch = torch
+        self.cfg = cfg
+        self.dist = dist
+        n = problem.n_coordinates
+        B = cfg.resolved_bucket_size()
+        layout = build_buckets(n, B)
+        if cfg.K * cfg.P > layout.n_buckets:
+            raise ValueError(f"K*P={cfg.K * cfg.P} exceeds the bucket count {layout.n_buckets}")
+        if cfg.K % dist.world != 0:
+            raise ValueError(f"K={cfg.K} node groups cannot be split over {dist.world} GPUs")
+        self.K_local = cfg.K // dist.world
+        self.node0 = dist.rank * self.K_local
+        node_part = static_node_partition(layout, cfg.K, RngStream(cfg.seed, (NODE_PARTITION,)))
+        nodes = node_part.assignment[self.node0:self.node0 + self.K_local]
+        for nb in nodes:
+            if cfg.P > len(nb):
+                raise ValueError("more threads than buckets on this node")
+        buckets = [b for nb in nodes for b in nb]
+        ptr = np.zeros(self.K_local + 1, dtype=np.int32)
+        np.cumsum([len(nb) for nb in nodes], out=ptr[1:])
+        if dist.world == 1:
+            store_cols = None
+            store_col = np.array([b * B for b in buckets], dtype=np.int64)
+            if problem._device is None:
+                problem._device = DeviceProblem(problem, dist=dist)
+            self.dp = problem._device
+        else:
+            lens = [layout.range_of(b)[1] - layout.range_of(b)[0] for b in buckets]
+            store_col = np.zeros(len(buckets), dtype=np.int64)
+            np.cumsum(lens[:-1], out=store_col[1:])
+            store_cols = np.concatenate([np.arange(*layout.range_of(b)) for b in buckets])
+            self.dp = DeviceProblem(problem, store_cols=store_cols, dist=dist)
+        dp = self.dp
+        self.single = cfg.K == 1 and cfg.P == 1
+        if self.single and dp.kind == LOGISTIC:
+            raise NotImplementedError(
+                "K=P=1 primal logistic uses the exact Newton path (solvers.py:403-410), "
+                "which is not on the GPU yet; use K*P > 1 or a quadratic objective")
+        self.a = dp.gamma * cfg.P * cfg.K
+        self.n_parts_local = self.K_local * cfg.P
+        # planning
+        self._ptr_host = ptr
+        self._buckets_dev = torch.from_numpy(np.asarray(buckets, dtype=np.int32)).cuda()
+        self._store_col_dev = torch.from_numpy(store_col).cuda()
+        self.desc = PlanDesc()
+        self.desc.seed = int(cfg.seed)
+        self.desc.n_global = int(n)
+        self.desc.bucket_size = int(B)
+        self.desc.n_nodes_local = int(self.K_local)
+        self.desc.node0 = int(self.node0)
+        self.desc.P = int(cfg.P)
+        self.desc.T3 = -1 if cfg.T3 is None else int(cfg.T3)
+        self.desc.T4 = -1 if cfg.T4 is None else int(cfg.T4)
+        self.desc.sampling = 0 if cfg.sampling == "perm" else 1
+        self.desc.repartition = 0 if cfg.repartition == "dynamic" else 1
+        self._ptr_c = (ctypes.c_int32 * (self.K_local + 1))(*ptr.tolist())
+        self.desc.node_bucket_ptr = self._ptr_c
+        self.desc.node_buckets = self._buckets_dev.data_ptr()
+        self.desc.bucket_store_col = self._store_col_dev.data_ptr()
+        L = lib()
+        self.stride = int(L.syscd_plan_max_updates(ctypes.byref(self.desc)))
+        if self.stride < 0:
+            call("syscd_plan_max_updates")
+        self.R = max(1, min(cfg.plan_batch, cfg.n_rounds * cfg.T2 if cfg.n_rounds else 1))
+        ws = int(L.syscd_plan_workspace_bytes(ctypes.byref(self.desc), self.R))
+        self.seq = torch.empty(self.R * max(1, self.stride), dtype=torch.int32, device="cuda")
+        self.wp = torch.empty(self.R * (self.n_parts_local + 1), dtype=torch.int64, device="cuda")
+        self.ws = torch.empty(max(ws, 256), dtype=torch.uint8, device="cuda")
+        self.planned = (None, None)  # [rid_lo, rid_hi)
+        # workers
+        d = dp.d
+        if dp.storage == "dense":
+            counts = {self.n_parts_local, cfg.P}
+            self.n_workers = max(self._dense_workers(d, c)[0] for c in counts)
+            self.cluster = self._dense_workers(d, self.n_parts_local)[1]
+            self.part_ld = (d + 31) // 32 * 32
+            self.partials = torch.empty(self.n_workers * self.part_ld, dtype=torch.float32,
+                                        device="cuda")
+        else:
+            nw = ctypes.c_int32(0)
+            call("syscd_sparse_epoch_workers", d, self.n_parts_local, ctypes.byref(nw))
+            self.n_workers = nw.value
+            self.cluster = 1
+            self.dv_work = torch.zeros(self.n_workers * d, dtype=torch.float32, device="cuda")
+            self.part_ld = d
+            self.partials = torch.empty(d, dtype=torch.float32, device="cuda")
+        self.alpha = torch.zeros(dp.n_store, dtype=torch.float32, device="cuda")
+        self.v = torch.zeros(d, dtype=torch.float64, device="cuda")
+        self.u = torch.empty(d, dtype=torch.float32, device="cuda")
+        self.dv = torch.empty(d, dtype=torch.float32, device="cuda")
+        self.status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        dp.grad_into(self.v, self.u)
+
+    @staticmethod
+    def _dense_workers(d, n_parts):
+        nw = ctypes.c_int32(0)
+        cl = ctypes.c_int32(0)
+        call("syscd_dense_epoch_workers", d, n_parts, ctypes.byref(nw), ctypes.byref(cl))
+        return nw.value, cl.value
+
+    # -- one device round (rid) over node range [k0, k1) with lin_vec u -------
+    def _ensure_plan(self, rid):
+        lo, hi = self.planned
+        if lo is not None and lo <= rid < hi:
+            return rid - lo
+        n = self.R
+        call("syscd_plan", ctypes.byref(self.desc), int(rid), n, _ptr(self.seq), self.stride,
+             _ptr(self.wp), _ptr(self.ws), self.ws.numel(), _stream())
+        self.planned = (rid, rid + n)
+        return 0
+
+    def round_tables(self, rid):
+        r = self._ensure_plan(rid)
+        seq = self.seq[r * self.stride:]
+        wp = self.wp[r * (self.n_parts_local + 1):(r + 1) * (self.n_parts_local + 1)]
+        return seq, wp
+
+    def epoch(self, rid, u, node_lo=0, node_hi=None):
+        """Run the partitions of local nodes [node_lo, node_hi) of round rid with
+        lin_vec u; leaves their summed replicas in self.dv."""
+        cfg, dp = self.cfg, self.dp
+        node_hi = self.K_local if node_hi is None else node_hi
+        seq, wp = self.round_tables(rid)
+        p0 = node_lo * cfg.P
+        nparts = (node_hi - node_lo) * cfg.P
+        wp_ptr = ctypes.c_void_p(wp.data_ptr() + 8 * p0)
+        if dp.storage == "dense":
+            e = DenseEpochArgs()
+            e.kind = dp.kind
+            e.d = dp.d
+            e.lda = dp.lda
+            e.A = dp.At.data_ptr()
+            e.sq = dp.sq.data_ptr()
+            e.alpha = self.alpha.data_ptr()
+            e.u = u.data_ptr()
+            e.seq = seq.data_ptr()
+            e.work_prefix = wp_ptr.value
+            e.n_parts = nparts
+            e.a = self.a
+            e.lam = dp.lam
+            e.n_coords = dp.n_coords
+            e.iid = 1 if cfg.sampling == "iid" else 0
+            e.n_store = dp.n_store
+            e.partials = self.partials.data_ptr()
+            e.part_ld = self.part_ld
+            e.status = self.status.data_ptr()
+            call("syscd_dense_epoch", ctypes.byref(e), _stream())
+            nw = self._dense_workers(dp.d, nparts)[0]
+            call("syscd_reduce_partials", _ptr(self.partials), self.part_ld, nw, dp.d,
+                 _ptr(self.dv), _stream())
+        else:
+            cp, ri, va = dp.csc
+            e = SparseEpochArgs()
+            e.kind = dp.kind
+            e.d = dp.d
+            e.col_ptr = cp.data_ptr()
+            e.row_idx = ri.data_ptr()
+            e.vals = va.data_ptr()
+            e.sq = dp.sq.data_ptr()
+            e.alpha = self.alpha.data_ptr()
+            e.u = u.data_ptr()
+            e.seq = seq.data_ptr()
+            e.work_prefix = wp_ptr.value
+            e.n_parts = nparts
+            e.a = self.a
+            e.lam = dp.lam
+            e.n_coords = dp.n_coords
+            e.iid = 1 if cfg.sampling == "iid" else 0
+            e.dv_work = self.dv_work.data_ptr()
+            e.n_workers = self.n_workers
+            e.delta_v = self.dv.data_ptr()
+            e.status = self.status.data_ptr()
+            call("syscd_sparse_epoch", ctypes.byref(e), _stream())
+
+    def global_round(self, t1):
+        """One outer round (solvers.py:401-424)."""
+        cfg, dp = self.cfg, self.dp
+        torch = self.torch
+        if cfg.T2 == 1:
+            self.epoch(t1, self.u)
+            self.dist.allreduce_(self.dv)
+            call("syscd_apply_dv", dp.kind, dp.d, _ptr(self.dv), _ptr(self.v), _ptr(dp.y),
+                 dp.lam, dp.n_coords, _ptr(self.u), _stream())
+            return
+        # T2 > 1: node-local rounds with the drift term (solvers.py:373-398)
+        drift = cfg.K * dp.gamma
+        delta_sum = torch.zeros(dp.d, dtype=torch.float64, device="cuda")
+        u_k = torch.empty_like(self.u)
+        for k in range(self.K_local):
+            v_node = self.v.clone()
+            for t2 in range(cfg.T2):
+                rid = t1 * cfg.T2 + t2
+                if t2 == 0:
+                    u_k.copy_(self.u)
+                else:
+                    dp.grad_into(self.v, u_k, v_node=v_node, drift=drift)
+                self.epoch(rid, u_k, k, k + 1)
+                call("syscd_apply_dv", dp.kind, dp.d, _ptr(self.dv), _ptr(v_node), None, dp.lam,
+                     dp.n_coords, None, _stream())
+            delta_sum += v_node - self.v
+        self.dist.allreduce_(delta_sum)
+        self.v += delta_sum
+        dp.grad_into(self.v, self.u)
+
+    def updates_last_round(self, rid):
+        _, wp = self.round_tables(rid)
+        return int(wp[self.n_parts_local].item())
+
+    def check_status(self):
+        st = int(self.status.item())
+        if st & 2:
+            self.status.zero_()
+            raise NonFiniteUpdateError("non-finite coordinate update")
+
+    def census_ok(self, rid):
+        seq, wp = self.round_tables(rid)
+        tot = int(wp[self.n_parts_local].item())
+        s = seq[:tot]
+        return int(torch_unique_count(s)) == tot
+
+    def alpha_global(self):
+        """alpha in global coordinate order, fp64 host array."""
+        dp = self.dp
+        if self.dist.world == 1:
+            return self.alpha.double().cpu().numpy()
+        torch = self.torch
+        full = torch.zeros(dp.n_global, dtype=torch.float64, device="cuda")
+        full[torch.from_numpy(dp.store_cols).cuda()] = self.alpha.double()
+        self.dist.allreduce_(full)
+        return full.cpu().numpy()
+
+
+def torch_unique_count(t):
+    import torch
+    return torch.unique(t).numel()
+
+
+def run_syscd(problem, cfg, f_star=None, dist=None):
+    """Hierarchical bucketized SySCD on the GPU (solvers.py:337-453)."""
+    if cfg.algorithm != "syscd":
+        raise ValueError("config.algorithm must be 'syscd'")
+    return _run(problem, cfg, f_star, dist)
+
+
+def run_sequential_scd(problem, cfg, f_star=None, dist=None):
+    """Sequential SCD (solvers.py:181-211): the K=P=1 round with exact
+    updates, which is what run_syscd does for K=P=1 (solvers.py:403-410)."""
+    if cfg.algorithm != "sequential":
+        raise ValueError("config.algorithm must be 'sequential'")
+    if cfg.K != 1 or cfg.P != 1:
+        raise ValueError("sequential solver runs on one thread")
+    import dataclasses
+    return _run(problem, dataclasses.replace(cfg, algorithm="syscd"), f_star, dist)
+
+
+def run_wild_parallel_scd(problem, cfg, f_star=None):
+    raise NotImplementedError(
+        "the PASSCoDe-wild baseline (solvers.py:214-286) is outside this framework's scope "
+        "(SURVEY 2, row 4)")
+
+
+def run_solver(problem, cfg, f_star=None):
+    if cfg.algorithm == "sequential":
+        return run_sequential_scd(problem, cfg, f_star=f_star)
+    if cfg.algorithm == "wild":
+        return run_wild_parallel_scd(problem, cfg, f_star=f_star)
+    return run_syscd(problem, cfg, f_star=f_star)
+
+
+def _rel_change(alpha, prev):
+    return float((alpha - prev).abs().max() / max(1.0, float(alpha.abs().max())))
+
+
+def _run(problem, cfg, f_star, dist):
+    torch = _torch()
+    dist = dist or Dist()
+    eng = _Engine(problem, cfg, dist)
+    dp = eng.dp
+
+    def metrics_row(epoch, secs, upd, rel):
+        if cfg.compute_gap:
+            gap, obj = dp.gap(eng.alpha)
+        else:
+            obj, gap = dp.objective(eng.alpha), None
+        sub = obj - f_star if f_star is not None else None
+        return EpochMetrics(epoch, obj, sub, secs, upd, rel, gap)
+
+    metrics = [metrics_row(0, 0.0, 0, np.inf)]
+    snaps = []
+    prev = eng.alpha.clone()
+    converged = diverged = False
+    total = 0
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    for t1 in range(cfg.n_rounds):
+        start.record()
+        eng.global_round(t1)
+        stop.record()
+        stop.synchronize()
+        elapsed = start.elapsed_time(stop) / 1e3
+        eng.check_status()
+        upd = 0
+        for t2 in range(cfg.T2):
+            upd += eng.updates_last_round(t1 * cfg.T2 + t2)
+        upd_t = torch.tensor([upd], dtype=torch.int64, device="cuda")
+        upd = int(dist.allreduce_(upd_t).item())
+        total += upd
+        if cfg.verify:
+            for t2 in range(cfg.T2):
+                if cfg.sampling == "perm" and not eng.census_ok(t1 * cfg.T2 + t2):
+                    raise AssertionError("write census: coordinate updated twice in one round")
+            vv = dp.matvec(eng.alpha)
+            scale = max(1.0, float(vv.abs().max()))
+            # fp32 replicas: relative consistency 1e-4 instead of the fp64 1e-8
+            if float((vv - eng.v).abs().max()) > 1e-4 * scale:
+                raise AssertionError("replica consistency: v != A @ alpha after reduction")
+        finite = torch.tensor([float(torch.isfinite(eng.alpha).all())], device="cuda")
+        if float(dist.allreduce_(finite, op="sum")) < dist.world:
+            metrics.append(EpochMetrics(t1 + 1, np.inf, None, elapsed, upd, np.inf))
+            diverged = True
+            break
+        d_rel = (eng.alpha - prev).abs().max().double().reshape(1)
+        m_abs = eng.alpha.abs().max().double().reshape(1)
+        dist.allreduce_(d_rel, op="max")
+        dist.allreduce_(m_abs, op="max")
+        rel = float(d_rel) / max(1.0, float(m_abs))
+        prev.copy_(eng.alpha)
+        last = t1 == cfg.n_rounds - 1
+        stop_now = cfg.T1 is None and rel < cfg.tolerance
+        if (t1 + 1) % cfg.metrics_every == 0 or last or stop_now:
+            metrics.append(metrics_row(t1 + 1, elapsed, upd, rel))
+        if cfg.record_alpha:
+            snaps.append(eng.alpha_global())
+        if stop_now:
+            converged = True
+            break
+    return TrainResult(eng.alpha_global(), metrics, converged, total, diverged=diverged,
+                       reason="diverged" if diverged else None, alpha_snapshots=snaps)
