@@ -79,6 +79,34 @@ __device__ __forceinline__ double coord_step(int kind, double lin, double a, dou
   }
 }
 
+// fp32 closed-form steps (ridge / primal-logistic surrogate / lasso / svm):
+// the inputs are fp32, so IEEE fp32 division keeps the step within an ulp of
+// the fp64 evaluation while staying off the fp64 pipe.
+__device__ __forceinline__ float coord_step_f(int kind, float lin, float a, float q, float lam,
+                                             float alpha, float inv_n) {
+  const float aq = a * q;
+  switch (kind) {
+    case SYSCD_RIDGE:
+    case SYSCD_LOGISTIC:
+      return alpha - __fdiv_rn(lin + lam * alpha, aq + lam);
+    case SYSCD_LASSO: {
+      if (aq <= 0.f) return 0.f;
+      const float z = alpha - __fdiv_rn(lin, aq);
+      const float m = fabsf(z) - __fdiv_rn(lam, aq);
+      return m > 0.f ? copysignf(m, z) : 0.f;
+    }
+    default: {  // SVM dual
+      if (aq <= 0.f) return 1.f;
+      const float z = alpha - __fdiv_rn(lin - inv_n, aq);
+      return fminf(fmaxf(z, 0.f), 1.f);
+    }
+  }
+}
+
+__device__ __forceinline__ void red_add_f32(float* p, float v) {
+  asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // PTX wrappers
 // ---------------------------------------------------------------------------

@@ -26,6 +26,9 @@
 //  * clusters process disjoint contiguous ranges of partitions (balanced by
 //    update count) and accumulate their partitions' replicas into one
 //    partials row each, in a fixed order: the result is deterministic.
+#include <stdio.h>
+#include <stdlib.h>
+
 #include <algorithm>
 #include <mutex>
 
@@ -46,6 +49,8 @@ struct DenseArgs {
   float a;
   double a_d;
   double lam;
+  float lam_f;
+  float inv_n_f;
   double n_coords;
   int32_t kind;
   int32_t iid;
@@ -55,9 +60,16 @@ struct DenseArgs {
   float* partials;
   int64_t part_ld;
   int32_t* status;
+  unsigned long long* dbg;  // optional per-step phase timestamps (CTA 0, thread 0)
 };
 
 constexpr int kMetaRing = 64;
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 constexpr int kMaxCluster = 16;
 
 template <int NTC, int RC, int NCH>
@@ -88,12 +100,14 @@ __host__ __device__ inline SmemLayout smem_layout(int stages, int chunk_rows) {
   o += (size_t)stages * 8;
   L.xbar = o;
   o += 2 * 8;
+  o = align_up(o, 16);
   L.slots = o;
   o += 2 * kMaxCluster * 4;
   L.red = o;
   o += 2 * 32 * 4;
+  o = align_up(o, 16);
   L.meta = o;
-  o += kMetaRing * 4;
+  o += kMetaRing * 16;
   L.range = o;
   o += 4 * 8;
   L.total = align_up(o, 128);
@@ -132,7 +146,7 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
   uint64_t* xbar = reinterpret_cast<uint64_t*>(smem + L.xbar);
   float* slots = reinterpret_cast<float*>(smem + L.slots);
   float* red = reinterpret_cast<float*>(smem + L.red);
-  int* meta = reinterpret_cast<int*>(smem + L.meta);
+  int4* meta = reinterpret_cast<int4*>(smem + L.meta);
   int64_t* range = reinterpret_cast<int64_t*>(smem + L.range);
 
   const int tid = threadIdx.x;
@@ -146,6 +160,7 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
   const int64_t d = args.d;
 
   for (int i = tid; i < S * CHUNK; i += blockDim.x) ring[i] = 0.f;
+  for (int i = tid; i < 2 * kMaxCluster; i += blockDim.x) slots[i] = 0.f;
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
@@ -168,6 +183,17 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
   __syncthreads();
   cluster_sync_all();
 
+  // bytes of each of this CTA's chunks (identical for every column); the tail
+  // of a partial chunk is never written, so with S % NCH == 0 (a stage always
+  // holds the same chunk index) it stays zero from the initial clear and rows
+  // past d contribute x = 0 without any per-row predicate.
+  uint32_t chunk_bytes[NCH];
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    int64_t valid = d - (row0 + (int64_t)c * CHUNK);
+    valid = valid < 0 ? 0 : (valid > CHUNK ? CHUNK : valid);
+    chunk_bytes[c] = (uint32_t)(((valid + 3) / 4) * 16);
+  }
   const int64_t p_lo = range[0];
   const int64_t p_hi = range[1];
   const int64_t s_begin = args.wp[p_lo];
@@ -176,7 +202,7 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
   if (warp == NWC) {
     // ------------------------------------------------------------ producer
     const uint64_t policy = args.evict_first ? policy_evict_first() : policy_evict_last();
-    uint32_t cc = 0;
+    uint32_t stage = 0, phase = 0;
     int jreg = 0;
     for (int64_t s = s_begin; s < s_end; ++s) {
       const int64_t rel = s - s_begin;
@@ -186,22 +212,26 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
       }
       const int j = __shfl_sync(0xffffffffu, jreg, (int)(rel & 31));
       if (lane == 0) {
-        const float* col = args.A + (int64_t)j * args.lda;
+        const float* col = args.A + (int64_t)j * args.lda + row0;
+        // perm mode: alpha_j is only written by this cluster, at this step,
+        // so it can be read ahead of time (iid re-reads it after the exchange)
+        const float aj = args.iid ? 0.f : args.alpha[j];
+        const float qj = __ldg(args.sq + j);
 #pragma unroll 1
-        for (int c = 0; c < NCH; ++c, ++cc) {
-          const uint32_t stage = cc % (uint32_t)S;
-          const uint32_t use = cc / (uint32_t)S;
-          mbar_wait(&empty[stage], (use & 1u) ^ 1u);
-          if (c == 0) meta[s & (kMetaRing - 1)] = j;
-          const int64_t r0 = row0 + (int64_t)c * CHUNK;
-          int64_t valid = d - r0;
-          valid = valid < 0 ? 0 : (valid > CHUNK ? CHUNK : valid);
-          const uint32_t bytes = (uint32_t)(((valid + 3) / 4) * 16);
+        for (int c = 0; c < NCH; ++c) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          if (c == 0)
+            meta[s & (kMetaRing - 1)] = make_int4(j, __float_as_int(aj), __float_as_int(qj), 0);
+          const uint32_t bytes = chunk_bytes[c];
           if (bytes) {
             mbar_arrive_expect_tx(&full[stage], bytes);
-            tma_load_1d(ring + (size_t)stage * CHUNK, col + r0, bytes, &full[stage], policy);
+            tma_load_1d(ring + (size_t)stage * CHUNK, col + c * CHUNK, bytes, &full[stage], policy);
           } else {
             mbar_arrive(&full[stage]);
+          }
+          if (++stage == (uint32_t)S) {
+            stage = 0;
+            phase ^= 1u;
           }
         }
       }
@@ -210,7 +240,7 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
   } else {
     // ------------------------------------------------------------ consumers
     // owned row of register slot q = c*RC + k is row0 + q*NTC + tid; slots
-    // q >= qmax lie past d and stay zero (their staged values are ignored).
+    // q >= qmax lie past d: their w stays 0 and their staged x is 0.
     const int64_t rem = d - row0 - tid;
     const int qmax = rem <= 0 ? 0 : (int)min((int64_t)R, (rem + NTC - 1) / NTC);
     const float* ub = args.u + row0 + tid;
@@ -224,31 +254,46 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
     int64_t part = p_lo;
     while (part < p_hi && args.wp[part + 1] <= s_begin) ++part;
     int64_t part_end = part < p_hi ? args.wp[part + 1] : s_end;
-    uint32_t cc = 0;
+    uint32_t stage0 = 0, phase0 = 0;  // ring position of the current step's chunk 0
     // exchange addresses: slot[buf][rank] and xbar[buf] in peer `lane`
     uint32_t peer_slot = 0, peer_bar = 0;
     if (warp == 0 && lane < C) {
       peer_slot = cluster_map(smem_addr(slots + rank), (uint32_t)lane);
       peer_bar = cluster_map(smem_addr(&xbar[0]), (uint32_t)lane);
     }
+    const float* ring_t = ring + tid;
+    const bool dbg = args.dbg != nullptr && blockIdx.x == 0 && tid == 0;
     for (int64_t s = s_begin; s < s_end; ++s) {
       const uint32_t t = (uint32_t)(s - s_begin);
       const uint32_t buf = t & 1u;
-      float acc = 0.f;
+      if (dbg && t < 512) args.dbg[t * 6 + 0] = gtimer();
+      float acc0 = 0.f, acc1 = 0.f;
+      {
+        uint32_t st = stage0, ph = phase0;
 #pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        const uint32_t stage = (cc + c) % (uint32_t)S;
-        const uint32_t use = (cc + c) / (uint32_t)S;
-        mbar_wait(&full[stage], use & 1u);
-        const float* x = ring + (size_t)stage * CHUNK + tid;
+        for (int c = 0; c < NCH; ++c) {
+          mbar_wait(&full[st], ph);
+          const float* x = ring_t + (size_t)st * CHUNK;
 #pragma unroll
-        for (int k = 0; k < RC; ++k) acc = fmaf(x[k * NTC], w[c * RC + k], acc);
+          for (int k = 0; k < RC; ++k) {
+            if (k & 1) {
+              acc1 = fmaf(x[k * NTC], w[c * RC + k], acc1);
+            } else {
+              acc0 = fmaf(x[k * NTC], w[c * RC + k], acc0);
+            }
+          }
+          if (++st == (uint32_t)S) {
+            st = 0;
+            ph ^= 1u;
+          }
+        }
       }
-      const int j = meta[s & (kMetaRing - 1)];
-      float aj = 0.f;
-      if (!args.iid) aj = args.alpha[j];
-      const float qj = args.sq[j];
-      acc = warp_sum(acc);
+      if (dbg && t < 512) args.dbg[t * 6 + 1] = gtimer();
+      const int4 mt = meta[s & (kMetaRing - 1)];
+      const int j = mt.x;
+      float aj = __int_as_float(mt.y);
+      const float qj = __int_as_float(mt.z);
+      float acc = warp_sum(acc0 + acc1);
       if (lane == 0) red[buf * 32 + warp] = acc;
       named_bar_sync(1, NTC);
       if (warp == 0) {
@@ -257,15 +302,26 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
         if (lane < C) st_async_f32(peer_slot + buf * kMaxCluster * 4, v, peer_bar + buf * 8);
         if (lane == 0) mbar_arrive_expect_tx(&xbar[buf], 4u * (uint32_t)C);
       }
-      mbar_wait_cluster(&xbar[buf], (t >> 1) & 1u);
-      float lin = 0.f;
-      for (int r = 0; r < C; ++r) lin += slots[buf * kMaxCluster + r];
+      if (dbg && t < 512) args.dbg[t * 6 + 2] = gtimer();
+      mbar_wait(&xbar[buf], (t >> 1) & 1u);
+      if (dbg && t < 512) args.dbg[t * 6 + 3] = gtimer();
+      float lin;
+      {
+        const float4* sl = reinterpret_cast<const float4*>(slots + buf * kMaxCluster);
+        const float4 s0 = sl[0], s1 = sl[1], s2 = sl[2], s3 = sl[3];
+        lin = ((s0.x + s0.y) + (s0.z + s0.w)) + ((s1.x + s1.y) + (s1.z + s1.w)) +
+              (((s2.x + s2.y) + (s2.z + s2.w)) + ((s3.x + s3.y) + (s3.z + s3.w)));
+      }
       if (args.iid) aj = *(volatile float*)(args.alpha + j);
-      const double anew = coord_step(args.kind, (double)lin, args.a_d, (double)qj, args.lam,
-                                     (double)aj, args.n_coords);
+      float an;
+      if (args.kind == SYSCD_LOGISTIC_DUAL) {
+        an = (float)coord_step(args.kind, (double)lin, args.a_d, (double)qj, args.lam, (double)aj,
+                               args.n_coords);
+      } else {
+        an = coord_step_f(args.kind, lin, a, qj, args.lam_f, aj, args.inv_n_f);
+      }
       float delta;
-      if (isfinite(anew)) {
-        const float an = (float)anew;
+      if (isfinite(an)) {
         delta = an - aj;
         if (rank == 0 && tid == 0) args.alpha[j] = an;
       } else {
@@ -273,28 +329,46 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
         if (rank == 0 && tid == 0) atomicOr(args.status, SYSCD_ENONFINITE);
       }
       const float sd = a * delta;
+      if (dbg && t < 512) args.dbg[t * 6 + 4] = gtimer();
 #pragma unroll
       for (int c = 0; c < NCH; ++c) {
-        const uint32_t stage = (cc + c) % (uint32_t)S;
-        const float* x = ring + (size_t)stage * CHUNK + tid;
+        const float* x = ring_t + (size_t)stage0 * CHUNK;
 #pragma unroll
-        for (int k = 0; k < RC; ++k) {
-          const int q = c * RC + k;
-          if (q < qmax) w[q] = fmaf(sd, x[k * NTC], w[q]);
-        }
+        for (int k = 0; k < RC; ++k) w[c * RC + k] = fmaf(sd, x[k * NTC], w[c * RC + k]);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (lane == 0) mbar_arrive(&empty[stage0]);
+        if (++stage0 == (uint32_t)S) {
+          stage0 = 0;
+          phase0 ^= 1u;
+        }
       }
-      cc += NCH;
+      if (dbg && t < 512) args.dbg[t * 6 + 5] = gtimer();
       if (s + 1 == part_end) {
-        // fold this partition's replica (w - u)/a into the cluster's partial sum
+        // fold this partition's replica (w - u)/a into the cluster's partial
+        // sum: plain store for the first partition, then fire-and-forget
+        // red.global.add (same thread, same address: applied in program
+        // order, so the sum stays deterministic); u comes through the
+        // read-only path so the loads issue back to back.
 #pragma unroll
-        for (int q = 0; q < R; ++q) {
-          if (q < qmax) {
-            const float uu = ub[q * NTC];
-            const float dv = (w[q] - uu) * inv_a;
-            out[q * NTC] = flushed ? out[q * NTC] + dv : dv;
-            w[q] = uu;
+        for (int c = 0; c < NCH; ++c) {
+          float uu[RC];
+#pragma unroll
+          for (int k = 0; k < RC; ++k) {
+            const int q = c * RC + k;
+            uu[k] = q < qmax ? __ldg(ub + q * NTC) : 0.f;
+          }
+#pragma unroll
+          for (int k = 0; k < RC; ++k) {
+            const int q = c * RC + k;
+            if (q < qmax) {
+              const float dv = (w[q] - uu[k]) * inv_a;
+              if (flushed) {
+                red_add_f32(out + q * NTC, dv);
+              } else {
+                out[q * NTC] = dv;
+              }
+              w[q] = uu[k];
+            }
           }
         }
         flushed = true;
@@ -353,8 +427,7 @@ static int choose_stages(const KernelEntry& e, size_t smem_budget) {
   const size_t fixed = smem_layout(0, e.ntc * e.rc).total + 1024;
   int s = (int)((smem_budget - fixed) / (stage_bytes + 16));
   s = std::min(s, 32);
-  s = s / e.nch * e.nch;
-  return s;
+  return s / e.nch * e.nch;  // a stage always holds the same chunk index
 }
 
 static int query_max_clusters(KernelEntry& e, int C, int stages, size_t smem) {
@@ -374,6 +447,9 @@ static int query_max_clusters(KernelEntry& e, int C, int stages, size_t smem) {
   cfg.numAttrs = 1;
   int n = 0;
   cudaError_t err = cudaOccupancyMaxActiveClusters(&n, e.fn, &cfg);
+  if (getenv("SYSCD_DEBUG"))
+    fprintf(stderr, "[syscd] cfg (%d,%d,%d) C=%d smem=%zu -> clusters=%d (%s)\n", e.ntc, e.rc,
+            e.nch, C, smem, n, cudaGetErrorString(err));
   if (err != cudaSuccess || n <= 0) {
     cudaGetLastError();
     n = -1;
@@ -399,7 +475,7 @@ static int choose(int64_t d, int32_t n_parts, Choice* out) {
   SYSCD_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   SYSCD_CUDA_TRY(
       cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  const size_t budget = (size_t)std::min(smem_optin, 200 * 1024);
+  const size_t budget = (size_t)smem_optin - 1024;
   double best = 1e300;
   Choice bc = {-1, 0, 0, 0, 0};
   for (int i = 0; i < kTableSize; ++i) {
@@ -436,6 +512,13 @@ static int choose(int64_t d, int32_t n_parts, Choice* out) {
 }  // namespace syscd
 
 using namespace syscd;
+
+static void* g_dbg_buffer = nullptr;
+// Debug hook (not part of the header ABI): when set to a device buffer of
+// >= 512*6 uint64, the next dense epochs record %globaltimer at the step
+// phases of CTA 0 (start, dot done, CTA reduce done, exchange done, step
+// done, axpy done).
+extern "C" void syscd_debug_set_timeline(void* device_buffer) { g_dbg_buffer = device_buffer; }
 
 extern "C" int syscd_dense_epoch_workers(int64_t d, int32_t n_parts, int32_t* n_workers,
                                          int32_t* cluster) {
@@ -483,6 +566,8 @@ extern "C" int syscd_dense_epoch(const syscd_dense_epoch_args* e, void* stream) 
   args.a = (float)e->a;
   args.a_d = e->a;
   args.lam = e->lam;
+  args.lam_f = (float)e->lam;
+  args.inv_n_f = (float)(1.0 / e->n_coords);
   args.n_coords = e->n_coords;
   args.kind = e->kind;
   args.iid = e->iid;
@@ -494,6 +579,7 @@ extern "C" int syscd_dense_epoch(const syscd_dense_epoch_args* e, void* stream) 
   args.partials = e->partials;
   args.part_ld = e->part_ld;
   args.status = e->status;
+  args.dbg = (unsigned long long*)g_dbg_buffer;
 
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ch.G * ch.C, 1, 1);

@@ -231,6 +231,8 @@ class _Engine:
         self.u = torch.empty(d, dtype=torch.float32, device="cuda")
         self.dv = torch.empty(d, dtype=torch.float32, device="cuda")
         self.status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.kernel_events = None  # (start, stop) CUDA events around the epoch kernel
+        self.launches = 0          # our kernel launches issued (bench accounting)
         dp.grad_into(self.v, self.u)
 
     @staticmethod
@@ -286,7 +288,11 @@ class _Engine:
             e.partials = self.partials.data_ptr()
             e.part_ld = self.part_ld
             e.status = self.status.data_ptr()
+            if self.kernel_events is not None:
+                self.kernel_events[0].record()
             call("syscd_dense_epoch", ctypes.byref(e), _stream())
+            if self.kernel_events is not None:
+                self.kernel_events[1].record()
             nw = self._dense_workers(dp.d, nparts)[0]
             call("syscd_reduce_partials", _ptr(self.partials), self.part_ld, nw, dp.d,
                  _ptr(self.dv), _stream())
@@ -312,7 +318,11 @@ class _Engine:
             e.n_workers = self.n_workers
             e.delta_v = self.dv.data_ptr()
             e.status = self.status.data_ptr()
+            if self.kernel_events is not None:
+                self.kernel_events[0].record()
             call("syscd_sparse_epoch", ctypes.byref(e), _stream())
+            if self.kernel_events is not None:
+                self.kernel_events[1].record()
 
     def global_round(self, t1):
         """One outer round (solvers.py:401-424)."""

@@ -1,0 +1,30 @@
+"""Per-step phase timeline of the dense epoch kernel (CTA 0)."""
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from paper_1911_07722_b200._lib import lib
+from paper_1911_07722_b200.configs import workload
+from paper_1911_07722_b200.device import Dist
+from paper_1911_07722_b200.solvers import _Engine
+cfg_id = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+torch.cuda.set_device(0)
+wl = workload(cfg_id)
+eng = _Engine(wl.problem, wl.solver, Dist())
+for t in range(3):
+    eng.global_round(t)
+buf = torch.zeros(512 * 6, dtype=torch.int64, device="cuda")
+L = lib(); L.syscd_debug_set_timeline.argtypes = [ctypes.c_void_p]
+L.syscd_debug_set_timeline(buf.data_ptr())
+eng.global_round(3)
+torch.cuda.synchronize()
+L.syscd_debug_set_timeline(None)
+t = buf.view(512, 6).cpu().numpy().astype(np.float64)
+t = t[t[:, 0] > 0]
+d = np.diff(t, axis=1)
+step = np.diff(t[:, 0])
+names = ["dot(wait+pass)", "cta_reduce+push", "exchange_wait", "step", "axpy(+release)"]
+print(f"steps recorded {len(t)}; mean step {step.mean():.0f} ns (median {np.median(step):.0f})")
+for i, nm in enumerate(names):
+    print(f"  {nm:18s} mean {d[:, i].mean():7.0f} ns  median {np.median(d[:, i]):7.0f}  p90 {np.percentile(d[:, i], 90):7.0f}")
+tail = t[1:, 0] - t[:-1, 5]
+print(f"  {'flush/loop':18s} mean {tail.mean():7.0f} ns  median {np.median(tail):7.0f}  max {tail.max():7.0f}")
