@@ -26,14 +26,8 @@ import numpy as np
 from ._lib import DenseEpochArgs, PlanDesc, SparseEpochArgs, call, lib
 from .device import DeviceProblem, Dist, _ptr, _stream, _torch
 from .objective import LOGISTIC, NonFiniteUpdateError
-from .partitioning import (
-    DEFAULT_CACHE_LINE_BYTES,
-    NODE_PARTITION,
-    RngStream,
-    build_buckets,
-    default_bucket_size,
-    static_node_partition,
-)
+from .partitioning import DEFAULT_CACHE_LINE_BYTES, default_bucket_size
+from .sharding import shard_plan
 
 DIVERGENCE_FACTOR = 1e6
 
@@ -145,33 +139,19 @@ class _Engine:
         self.dist = dist
         n = problem.n_coordinates
         B = cfg.resolved_bucket_size()
-        layout = build_buckets(n, B)
-        if cfg.K * cfg.P > layout.n_buckets:
-            raise ValueError(f"K*P={cfg.K * cfg.P} exceeds the bucket count {layout.n_buckets}")
-        if cfg.K % dist.world != 0:
-            raise ValueError(f"K={cfg.K} node groups cannot be split over {dist.world} GPUs")
-        self.K_local = cfg.K // dist.world
-        self.node0 = dist.rank * self.K_local
-        node_part = static_node_partition(layout, cfg.K, RngStream(cfg.seed, (NODE_PARTITION,)))
-        nodes = node_part.assignment[self.node0:self.node0 + self.K_local]
-        for nb in nodes:
-            if cfg.P > len(nb):
-                raise ValueError("more threads than buckets on this node")
-        buckets = [b for nb in nodes for b in nb]
-        ptr = np.zeros(self.K_local + 1, dtype=np.int32)
-        np.cumsum([len(nb) for nb in nodes], out=ptr[1:])
-        if dist.world == 1:
-            store_cols = None
-            store_col = np.array([b * B for b in buckets], dtype=np.int64)
+        sp = shard_plan(n, B, cfg.K, cfg.P, cfg.seed, dist.world, dist.rank)
+        self.shard = sp
+        self.K_local = sp.K_local
+        self.node0 = sp.node0
+        buckets = sp.buckets
+        ptr = sp.node_ptr
+        store_col = sp.bucket_store_col
+        if sp.store_cols is None:
             if problem._device is None:
                 problem._device = DeviceProblem(problem, dist=dist)
             self.dp = problem._device
         else:
-            lens = [layout.range_of(b)[1] - layout.range_of(b)[0] for b in buckets]
-            store_col = np.zeros(len(buckets), dtype=np.int64)
-            np.cumsum(lens[:-1], out=store_col[1:])
-            store_cols = np.concatenate([np.arange(*layout.range_of(b)) for b in buckets])
-            self.dp = DeviceProblem(problem, store_cols=store_cols, dist=dist)
+            self.dp = DeviceProblem(problem, store_cols=sp.store_cols, dist=dist)
         dp = self.dp
         self.single = cfg.K == 1 and cfg.P == 1
         if self.single and dp.kind == LOGISTIC:

@@ -1,0 +1,102 @@
+"""Host-side API contract (no GPU): SolverConfig validation (solvers.py:63-79,
+test_solvers.py:210-228), problem validation and objective-kind mapping,
+reduce_replicas order (test_solvers.py:27-54), sharding."""
+import numpy as np
+import pytest
+
+from paper_1911_07722_b200 import (
+    COORDINATES_ARE_EXAMPLES,
+    ColumnMatrix,
+    DatasetStats,
+    GlmProblem,
+    LabeledDataset,
+    Regularizer,
+    SmoothLoss,
+    SolverConfig,
+    reduce_replicas,
+)
+from paper_1911_07722_b200.objective import LASSO, LOGISTIC, LOGISTIC_DUAL, RIDGE, SVM_DUAL
+from paper_1911_07722_b200.sharding import shard_plan
+
+
+def test_config_validation():
+    for kw in (dict(K=0), dict(P=0), dict(T2=0), dict(T3=0), dict(T4=0), dict(sampling="sobol"),
+               dict(repartition="greedy"), dict(tolerance=0.0), dict(max_epochs=-1),
+               dict(algorithm="gradient_descent"), dict(metrics_every=0)):
+        with pytest.raises(ValueError):
+            SolverConfig(**kw)
+    assert SolverConfig(cache_line_bytes=128).resolved_bucket_size() == 16
+    assert SolverConfig().resolved_bucket_size() == 8
+    assert SolverConfig(T1=7).n_rounds == 7 and SolverConfig(max_epochs=9).n_rounds == 9
+
+
+def _stats(n):
+    return DatasetStats(np.ones(n), float("nan"), 1.0)
+
+
+def test_problem_kinds_and_validation():
+    m = ColumnMatrix(4, 3, dense=np.ones((4, 3)))
+    feat = LabeledDataset(m, np.array([1.0, -1, 1, -1]))
+    ex = LabeledDataset(m, np.array([1.0, -1, 1]), COORDINATES_ARE_EXAMPLES)
+    assert GlmProblem(feat, SmoothLoss.squared_error(), Regularizer("l2", 1.0), _stats(3)).kind == RIDGE
+    assert GlmProblem(feat, SmoothLoss.squared_error(), Regularizer("l1", 1.0), _stats(3)).kind == LASSO
+    assert GlmProblem(feat, SmoothLoss.logistic(), Regularizer("l2", 1.0), _stats(3)).kind == LOGISTIC
+    svm = GlmProblem(ex, SmoothLoss.hinge(), Regularizer("l2", 0.5), _stats(3))
+    assert svm.kind == SVM_DUAL and svm.gamma == pytest.approx(1 / (0.5 * 9))
+    assert GlmProblem(ex, SmoothLoss.logistic(), Regularizer("l2", 1.0), _stats(3)).kind == LOGISTIC_DUAL
+    with pytest.raises(ValueError):
+        Regularizer("elastic", 1.0)
+    with pytest.raises(ValueError):
+        Regularizer("l2", 0.0)
+    with pytest.raises(ValueError):  # hinge needs the dual orientation
+        GlmProblem(feat, SmoothLoss.hinge(), Regularizer("l2", 1.0), _stats(3))
+    with pytest.raises(ValueError):  # squared loss has no dual row here
+        GlmProblem(ex, SmoothLoss.squared_error(), Regularizer("l2", 1.0), _stats(3))
+    with pytest.raises(ValueError):  # labels must be +-1 for logistic
+        GlmProblem(LabeledDataset(m, np.array([0.5, 1, 1, 1])), SmoothLoss.logistic(),
+                   Regularizer("l2", 1.0), _stats(3))
+    with pytest.raises(ValueError):
+        LabeledDataset(m, np.ones(5))
+
+
+def test_column_matrix_validation():
+    with pytest.raises(ValueError):
+        ColumnMatrix(2, 2, dense=np.array([[1.0, np.nan], [0, 1]]))
+    with pytest.raises(ValueError):
+        ColumnMatrix(3, 1, sparse_cols=[([2, 1], [1.0, 1.0])])
+    with pytest.raises(ValueError):
+        ColumnMatrix(3, 1, sparse_cols=[([0, 5], [1.0, 1.0])])
+    m = ColumnMatrix(3, 2, sparse_cols=[([0, 2], [1.0, 2.0]), ([1], [3.0])])
+    assert m.nnz() == 3
+    np.testing.assert_array_equal(m.to_dense(), [[1, 0], [0, 3], [2, 0]])
+
+
+def test_reduce_replicas_order_and_copy():
+    g = np.random.default_rng(0)
+    base = g.standard_normal(40)
+    reps = [base + g.standard_normal(40) * 0.1 for _ in range(5)]
+    got = reduce_replicas(base, reps)
+    exp = np.empty(40)
+    for i in range(40):
+        acc = 0.0
+        for r in reps:
+            acc += r[i] - base[i]
+        exp[i] = base[i] + acc
+    assert np.array_equal(got, exp)
+    one = np.array([1.0, -2.0, 3.0])
+    out = reduce_replicas(np.zeros(3), [one])
+    assert np.array_equal(out, one) and out is not one
+    with pytest.raises(ValueError):
+        reduce_replicas(np.zeros(3), [])
+    with pytest.raises(ValueError):
+        reduce_replicas(np.zeros(3), [np.zeros(4)])
+
+
+def test_shard_plan_single_and_errors(built_lib):
+    sp = shard_plan(100, 8, 1, 4, seed=3)
+    assert sp.store_cols is None and sorted(sp.buckets.tolist()) == list(range(13))
+    assert (sp.bucket_store_col == sp.buckets * 8).all()
+    with pytest.raises(ValueError, match="bucket count"):
+        shard_plan(16, 8, 2, 2, seed=0)
+    with pytest.raises(ValueError):
+        shard_plan(100, 8, 3, 1, seed=0, world=2, rank=0)

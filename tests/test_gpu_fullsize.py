@@ -1,0 +1,42 @@
+"""Full BASELINE sizes, checked through size-independent properties: the
+maintained shared vector equals a fresh A alpha (verify mode), descent, a
+non-negative shrinking duality gap, alpha in its box, determinism."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(cfg_id, epochs, **over):
+    import dataclasses
+    from paper_1911_07722_b200 import run_syscd
+    from paper_1911_07722_b200.configs import workload
+    wl = workload(cfg_id)
+    cfg = dataclasses.replace(wl.solver, T1=epochs, **over)
+    return wl, run_syscd(wl.problem, cfg)
+
+
+def test_config2_lasso_full_size(cuda):
+    wl, res = _run(2, 6, verify=True, compute_gap=True)
+    objs = [m.objective for m in res.metrics]
+    gaps = [m.gap for m in res.metrics]
+    assert all(b < a for a, b in zip(objs, objs[1:]))
+    assert all(g > 0 for g in gaps) and gaps[-1] < gaps[0]
+    assert all(m.updates == 2000 for m in res.metrics[1:])
+    _, res2 = _run(2, 6)
+    assert np.array_equal(res.alpha, res2.alpha)
+
+
+def test_config1_svm_full_size(cuda):
+    wl, res = _run(1, 3, compute_gap=True)
+    assert np.all((res.alpha >= 0) & (res.alpha <= 1))
+    objs = [m.objective for m in res.metrics]
+    assert objs[-1] < objs[0]
+    assert all(m.gap >= 0 for m in res.metrics) and res.metrics[-1].gap < res.metrics[0].gap
+    assert all(m.updates == 2_000_000 for m in res.metrics[1:])
+
+
+def test_config0_full_size_verify(cuda):
+    wl, res = _run(0, 20, verify=True)
+    objs = [m.objective for m in res.metrics]
+    assert all(b <= a for a, b in zip(objs, objs[1:]))

@@ -1,0 +1,189 @@
+"""GPU parity with the CPU oracle (same seeded data, partitioning and
+permutations): per-epoch objective within 1e-4 relative, final alpha within
+1e-3 relative L2 (north_star), across the five BASELINE configs at oracle
+sizes and every solver option the reference exposes."""
+import dataclasses
+
+import numpy as np
+import pytest
+
+from gpu_helpers import assert_parity, both
+from oracle import syscd_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def run_pair(cfg_id, scale, gap=True, **kw):
+    from paper_1911_07722_b200 import SolverConfig, run_syscd
+    pb, ob = both(cfg_id, scale)
+    seed = kw.pop("seed", 0)
+    res = run_syscd(pb, SolverConfig(seed=seed, compute_gap=gap, **kw))
+    ores = O.run_syscd(ob, O.OracleConfig(seed=seed, with_gap=gap, **kw))
+    return res, ores
+
+
+CASES = [
+    # config 0 geometry (ridge), reference partition settings and variants
+    (0, 0.05, dict(K=1, P=4, bucket_size=4, T1=6)),
+    (0, 0.05, dict(K=2, P=2, bucket_size=4, T1=6)),
+    (0, 0.05, dict(K=3, P=2, bucket_size=3, T1=5)),
+    (0, 0.05, dict(K=1, P=1, bucket_size=8, T1=5)),
+    (0, 0.05, dict(K=1, P=2, bucket_size=4, T2=3, T1=4)),
+    (0, 0.05, dict(K=2, P=2, bucket_size=4, T2=2, repartition="static", T1=4)),
+    (0, 0.05, dict(K=1, P=3, bucket_size=5, T3=2, T4=3, T1=4)),
+    (0, 0.05, dict(K=1, P=2, bucket_size=4, sampling="iid", T3=2, T4=3, T1=4)),
+    (0, 0.05, dict(K=1, P=5, bucket_size=1, T1=4)),
+    (0, 0.05, dict(K=1, P=2, bucket_size=25, T1=3)),
+    (0, 0.05, dict(K=1, P=1, bucket_size=100, T1=3)),  # bucket larger than n (one bucket)
+    # config 1 (svm dual), 2 (lasso), 3 (ridge), 4 (sparse logistic dual)
+    (1, 0.0005, dict(K=1, P=8, bucket_size=4, T1=4)),
+    (1, 0.0005, dict(K=2, P=4, bucket_size=32, T1=4)),
+    (2, 0.01, dict(K=1, P=4, bucket_size=2, T1=5)),
+    (2, 0.01, dict(K=1, P=1, bucket_size=8, T1=5)),
+    (3, 0.002, dict(K=1, P=2, bucket_size=8, T1=4)),
+    (4, 0.0002, dict(K=1, P=4, bucket_size=8, T1=4)),
+    (4, 0.0002, dict(K=2, P=3, bucket_size=16, sampling="iid", T3=3, T4=4, T1=3)),
+]
+
+
+@pytest.mark.parametrize("cfg_id,scale,kw", CASES)
+def test_trajectory_parity(cuda, cfg_id, scale, kw):
+    res, ores = run_pair(cfg_id, scale, **dict(kw))
+    assert_parity(res, ores)
+    for m, r in zip(res.metrics, ores.rows):
+        tol = 1e-4 * abs(r.objective) + 1e-3 * abs(r.gap) + 1e-9
+        assert abs(m.gap - r.gap) <= tol + 1e-4 * abs(ores.rows[0].objective)
+
+
+def test_full_size_config0_parity(cuda):
+    """BASELINE config 0 at full size (20000 x 500, K=1 P=4 B=16), 20 epochs."""
+    res, ores = run_pair(0, 1.0, gap=False, K=1, P=4, bucket_size=16, T1=20)
+    assert_parity(res, ores)
+
+
+def test_reference_golden_runs_on_gpu(cuda, golden):
+    """The reference's own trajectories (tests/golden/reference_runs.json)."""
+    from paper_1911_07722_b200 import (GlmProblem, SmoothLoss, SolverConfig,
+                                       generate_synthetic_dense, run_syscd)
+    for case in golden("reference_runs.json"):
+        ds = generate_synthetic_dense(case["n_rows"], case["n_cols"], case["data_seed"])
+        loss = SmoothLoss.squared_error() if case["loss"] == "squared_error" else SmoothLoss.logistic()
+        if case["loss"] == "logistic" and case["cfg"].get("K", 1) * case["cfg"].get("P", 1) == 1:
+            continue
+        pb = GlmProblem.build(ds, loss, case["lam"])
+        res = run_syscd(pb, SolverConfig(**case["cfg"]))
+        got = np.array([m.objective for m in res.metrics])
+        ref = np.array(case["objective"])
+        assert np.max(np.abs(got - ref) / np.abs(ref)) < 1e-4
+        assert [m.updates for m in res.metrics] == case["updates"]
+        a = np.array(case["alpha"])
+        assert np.linalg.norm(res.alpha - a) / np.linalg.norm(a) < 1e-3
+
+
+def test_extended_golden_runs_on_gpu(cuda, golden):
+    """Lasso / SVM-dual / logistic-dual trajectories of the reference driver."""
+    from paper_1911_07722_b200 import (COORDINATES_ARE_EXAMPLES, ColumnMatrix, GlmProblem,
+                                       LabeledDataset, Regularizer, SmoothLoss, SolverConfig,
+                                       run_syscd)
+    from paper_1911_07722_b200.dataset import compute_stats
+    for case in golden("extended_runs.json"):
+        A = np.array(case["A"])
+        d, n = A.shape
+        if case["kind"] == "lasso":
+            ds = LabeledDataset(ColumnMatrix(d, n, dense=A), np.array(case["y"]))
+            pb = GlmProblem(ds, SmoothLoss.squared_error(), Regularizer("l1", case["lam"]),
+                            compute_stats(ds.matrix))
+        else:
+            # fixtures store folded columns y_i x_i: present them with labels +1
+            ds = LabeledDataset(ColumnMatrix(d, n, dense=A), np.ones(n), COORDINATES_ARE_EXAMPLES)
+            loss = SmoothLoss.hinge() if case["kind"] == "svm_dual" else SmoothLoss.logistic()
+            pb = GlmProblem(ds, loss, Regularizer("l2", case["lam"]), compute_stats(ds.matrix))
+        res = run_syscd(pb, SolverConfig(**case["cfg"]))
+        got = np.array([m.objective for m in res.metrics])
+        ref = np.array(case["objective"])
+        floor = 1e-6 * max(np.max(np.abs(ref)), 1e-12)
+        assert np.max(np.abs(got - ref) / np.maximum(np.abs(ref), floor)) < 1e-4, case["kind"]
+        a = np.array(case["alpha"])
+        assert np.linalg.norm(res.alpha - a) / np.linalg.norm(a) < 1e-3
+
+
+def test_degenerate_equals_sequential(cuda):
+    from paper_1911_07722_b200 import SolverConfig, run_sequential_scd, run_syscd
+    pb, _ = both(0, 0.05)
+    n = pb.n_coordinates
+    seq = run_sequential_scd(pb, SolverConfig(algorithm="sequential", bucket_size=n, seed=7, T1=4,
+                                              record_alpha=True))
+    deg = run_syscd(pb, SolverConfig(K=1, P=1, bucket_size=n, T2=1, T3=1, T4=n, seed=7, T1=4,
+                                     record_alpha=True))
+    assert len(seq.alpha_snapshots) == 4
+    for a, b in zip(seq.alpha_snapshots, deg.alpha_snapshots):
+        assert np.array_equal(a, b)
+
+
+def test_determinism_and_seed(cuda):
+    from paper_1911_07722_b200 import SolverConfig, run_syscd
+    pb, _ = both(2, 0.02)
+    cfg = SolverConfig(K=2, P=2, bucket_size=4, seed=11, T1=6)
+    a, b = run_syscd(pb, cfg), run_syscd(pb, cfg)
+    assert np.array_equal(a.alpha, b.alpha)
+    assert [m.objective for m in a.metrics] == [m.objective for m in b.metrics]
+    c = run_syscd(pb, dataclasses.replace(cfg, seed=12))
+    assert not np.array_equal(a.alpha, c.alpha)
+
+
+def test_verify_mode_and_accounting(cuda):
+    from paper_1911_07722_b200 import SolverConfig, run_syscd
+    pb, _ = both(0, 0.05)
+    res = run_syscd(pb, SolverConfig(K=2, P=2, bucket_size=4, seed=8, T1=5, verify=True))
+    assert all(m.updates == pb.n_coordinates for m in res.metrics[1:])
+    assert res.total_updates == 5 * pb.n_coordinates and not res.diverged
+    iid = run_syscd(pb, SolverConfig(K=1, P=2, bucket_size=4, seed=12, sampling="iid", T1=3, T2=2,
+                                     T3=2, T4=5))
+    assert all(m.updates == 1 * 2 * 2 * 2 * 5 for m in iid.metrics[1:])
+
+
+def test_monotone_descent_parallel(cuda):
+    from paper_1911_07722_b200 import SolverConfig, run_syscd
+    pb, _ = both(0, 0.05)
+    res = run_syscd(pb, SolverConfig(K=2, P=2, bucket_size=4, seed=9, T1=15))
+    objs = [m.objective for m in res.metrics]
+    assert all(b <= a * (1 + 1e-6) for a, b in zip(objs, objs[1:]))
+
+
+def test_zero_epochs_and_tolerance_stop(cuda):
+    from paper_1911_07722_b200 import SolverConfig, run_syscd
+    pb, _ = both(0, 0.05)
+    r0 = run_syscd(pb, SolverConfig(K=1, P=2, bucket_size=4, max_epochs=0))
+    assert len(r0.metrics) == 1 and r0.total_updates == 0 and not r0.converged
+    assert np.array_equal(r0.alpha, np.zeros(pb.n_coordinates))
+    rt = run_syscd(pb, SolverConfig(K=1, P=1, bucket_size=4, tolerance=1e-4, max_epochs=500))
+    assert rt.converged and len(rt.metrics) - 1 < 500
+    rf = run_syscd(pb, SolverConfig(K=1, P=1, bucket_size=4, tolerance=1e-4, T1=3))
+    assert not rf.converged and len(rf.metrics) - 1 == 3
+
+
+def test_errors(cuda):
+    from paper_1911_07722_b200 import (ColumnMatrix, GlmProblem, LabeledDataset,
+                                       NonFiniteUpdateError, SmoothLoss, SolverConfig, run_solver,
+                                       run_syscd)
+    pb, _ = both(0, 0.01)  # 200 x 8 -> 2 buckets at B=4
+    with pytest.raises(ValueError, match="bucket count"):
+        run_syscd(pb, SolverConfig(K=2, P=2, bucket_size=4))
+    with pytest.raises(ValueError):
+        run_syscd(pb, SolverConfig(algorithm="sequential"))
+    with pytest.raises(NotImplementedError):
+        run_solver(pb, SolverConfig(algorithm="wild", T1=1))
+    big = np.full((64, 4), 3e38, dtype=np.float64)
+    ds = LabeledDataset(ColumnMatrix(64, 4, dense=big), np.ones(64))
+    bad = GlmProblem.build(ds, SmoothLoss.squared_error(), 1.0)
+    with pytest.raises(NonFiniteUpdateError):
+        run_syscd(bad, SolverConfig(K=1, P=2, bucket_size=2, T1=2))
+
+
+def test_dual_alpha_stays_in_box(cuda):
+    from paper_1911_07722_b200 import SolverConfig, run_syscd
+    for cfg_id, scale in [(1, 0.0005), (4, 0.0002)]:
+        pb, _ = both(cfg_id, scale)
+        res = run_syscd(pb, SolverConfig(K=1, P=4, bucket_size=8, T1=6, compute_gap=True))
+        assert np.all(res.alpha >= 0) and np.all(res.alpha <= 1)
+        assert all(m.gap >= -1e-6 for m in res.metrics)
