@@ -174,14 +174,14 @@ int syscd_sparse_epoch(const syscd_sparse_epoch_args* e, void* stream);
  * ------------------------------------------------------------------------ */
 int syscd_reduce_partials(const float* partials, int64_t part_ld, int32_t n_workers, int64_t d,
                           float* dv, void* stream);
-int syscd_apply_dv(int32_t kind, int64_t d, const float* dv, double* v, const float* y,
+int syscd_apply_dv(int32_t kind, int64_t d, const float* dv, double* v, const double* y,
                    double lam, double n_coords, float* u, void* stream);
 /* u = grad f(v) + drift * (v_node - v)   (solvers.py:379-382 for T2 > 1) */
-int syscd_grad(int32_t kind, int64_t d, const double* v, const float* y, double lam,
+int syscd_grad(int32_t kind, int64_t d, const double* v, const double* y, double lam,
                double n_coords, const double* v_node, double drift, float* u, void* stream);
 /* fp64 certificate point for the duality gap: primal kinds w = grad f(v),
  * dual kinds w = v / (lam n). */
-int syscd_dual_point(int32_t kind, int64_t d, const double* v, const float* y, double lam,
+int syscd_dual_point(int32_t kind, int64_t d, const double* v, const double* y, double lam,
                      double n_coords, double* w, void* stream);
 
 /* ------------------------------------------------------------------------
@@ -206,10 +206,10 @@ int syscd_sparse_col_sq_norms(int64_t n, const int64_t* col_ptr, const float* va
 /* Objective / gap terms (fp64).  out[0..7] (see paper_1911_07722_b200/metrics.py):
  *   mode 0: out[0] = f(v), out[1] = sum_j g(alpha_j)
  *   mode 1: dual-certificate terms for the gap given atw = A^T w.      */
-int syscd_objective_terms(int32_t kind, int64_t d, int64_t n, const double* v, const float* y,
+int syscd_objective_terms(int32_t kind, int64_t d, int64_t n, const double* v, const double* y,
                           const float* alpha, double lam, double n_coords, double* out,
                           double* work, void* stream);
-int syscd_gap_terms(int32_t kind, int64_t d, int64_t n, const double* v, const float* y,
+int syscd_gap_terms(int32_t kind, int64_t d, int64_t n, const double* v, const double* y,
                     const double* atw, double lam, double n_coords, double scale, double* out,
                     double* work, void* stream);
 

@@ -37,35 +37,35 @@ __global__ void k_reduce_partials(const float* __restrict__ partials, int64_t ld
 }
 
 __global__ void k_apply_dv(int kind, int64_t d, const float* __restrict__ dv, double* __restrict__ v,
-                           const float* __restrict__ y, double lam, double n, float* __restrict__ u) {
+                           const double* __restrict__ y, double lam, double n, float* __restrict__ u) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d;
        i += (int64_t)gridDim.x * blockDim.x) {
     const double nv = v[i] + (double)dv[i];
     v[i] = nv;
-    if (u) u[i] = (float)grad_of(kind, nv, y ? (double)y[i] : 0.0, lam, n);
+    if (u) u[i] = (float)grad_of(kind, nv, y ? y[i] : 0.0, lam, n);
   }
 }
 
-__global__ void k_grad(int kind, int64_t d, const double* __restrict__ v, const float* __restrict__ y,
+__global__ void k_grad(int kind, int64_t d, const double* __restrict__ v, const double* __restrict__ y,
                        double lam, double n, const double* __restrict__ v_node, double drift,
                        float* __restrict__ u) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d;
        i += (int64_t)gridDim.x * blockDim.x) {
-    double gval = grad_of(kind, v[i], y ? (double)y[i] : 0.0, lam, n);
+    double gval = grad_of(kind, v[i], y ? y[i] : 0.0, lam, n);
     if (v_node) gval += drift * (v_node[i] - v[i]);
     u[i] = (float)gval;
   }
 }
 
 __global__ void k_dual_point(int kind, int64_t d, const double* __restrict__ v,
-                             const float* __restrict__ y, double lam, double n,
+                             const double* __restrict__ y, double lam, double n,
                              double* __restrict__ w) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d;
        i += (int64_t)gridDim.x * blockDim.x) {
     if (kind == SYSCD_SVM_DUAL || kind == SYSCD_LOGISTIC_DUAL) {
       w[i] = v[i] / (lam * n);
     } else {
-      w[i] = grad_of(kind, v[i], y ? (double)y[i] : 0.0, lam, n);
+      w[i] = grad_of(kind, v[i], y ? y[i] : 0.0, lam, n);
     }
   }
 }
@@ -193,7 +193,7 @@ struct TermArgs {
   int mode, kind;
   int64_t d, n;
   const double* v;
-  const float* y;
+  const double* y;
   const float* alpha;
   const double* atw;
   double lam, ncoord, scale;
@@ -201,7 +201,7 @@ struct TermArgs {
 
 __device__ void row_terms(const TermArgs& a, int64_t i, double* t) {
   const double v = a.v[i];
-  const double y = a.y ? (double)a.y[i] : 0.0;
+  const double y = a.y ? a.y[i] : 0.0;
   if (a.mode == 0) {
     if (a.kind == SYSCD_RIDGE || a.kind == SYSCD_LASSO) {
       t[0] += 0.5 * (v - y) * (v - y);
@@ -318,7 +318,7 @@ extern "C" int syscd_reduce_partials(const float* partials, int64_t part_ld, int
   return SYSCD_OK;
 }
 
-extern "C" int syscd_apply_dv(int32_t kind, int64_t d, const float* dv, double* v, const float* y,
+extern "C" int syscd_apply_dv(int32_t kind, int64_t d, const float* dv, double* v, const double* y,
                               double lam, double n_coords, float* u, void* stream) {
   if (!dv || !v || d < 1) {
     set_error("syscd_apply_dv: invalid arguments");
@@ -330,7 +330,7 @@ extern "C" int syscd_apply_dv(int32_t kind, int64_t d, const float* dv, double* 
   return SYSCD_OK;
 }
 
-extern "C" int syscd_grad(int32_t kind, int64_t d, const double* v, const float* y, double lam,
+extern "C" int syscd_grad(int32_t kind, int64_t d, const double* v, const double* y, double lam,
                           double n_coords, const double* v_node, double drift, float* u,
                           void* stream) {
   if (!v || !u || d < 1) {
@@ -343,7 +343,7 @@ extern "C" int syscd_grad(int32_t kind, int64_t d, const double* v, const float*
   return SYSCD_OK;
 }
 
-extern "C" int syscd_dual_point(int32_t kind, int64_t d, const double* v, const float* y,
+extern "C" int syscd_dual_point(int32_t kind, int64_t d, const double* v, const double* y,
                                 double lam, double n_coords, double* w, void* stream) {
   if (!v || !w || d < 1) {
     set_error("syscd_dual_point: invalid arguments");
@@ -458,7 +458,7 @@ static int run_terms(const TermArgs& a, double* out, double* work, cudaStream_t 
 // is lam/2 * out[1]; lasso lam*out[1]; svm -out[1]/n; logistic-dual out[1]/n;
 // dual f = out[0] / (2 lam n^2)).  work: >= 296*4 doubles.
 extern "C" int syscd_objective_terms(int32_t kind, int64_t d, int64_t n, const double* v,
-                                     const float* y, const float* alpha, double lam,
+                                     const double* y, const float* alpha, double lam,
                                      double n_coords, double* out, double* work, void* stream) {
   if (!v || !alpha || d < 1 || n < 1) {
     set_error("syscd_objective_terms: invalid arguments");
@@ -472,7 +472,7 @@ extern "C" int syscd_objective_terms(int32_t kind, int64_t d, int64_t n, const d
 //  ridge/lasso: out[0]=|w|^2, out[1]=w.y, out[2]=|atw|^2 (ridge), out[3]=max|atw| (lasso)
 //  logistic:    out[0]=sum entropy(s), out[2]=|atw|^2
 //  svm/logdual: out[0]=|w|^2 (w = v/(lam n)), out[2]=sum hinge / log-loss of margins atw
-extern "C" int syscd_gap_terms(int32_t kind, int64_t d, int64_t n, const double* v, const float* y,
+extern "C" int syscd_gap_terms(int32_t kind, int64_t d, int64_t n, const double* v, const double* y,
                                const double* atw, double lam, double n_coords, double scale,
                                double* out, double* work, void* stream) {
   if (!v || !atw || d < 1 || n < 1) {

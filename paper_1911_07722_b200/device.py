@@ -199,7 +199,7 @@ class DeviceProblem:
             self.lda = None
         sq_full = problem.stats.column_sq_norms
         self.sq = torch.from_numpy(np.asarray(sq_full, dtype=np.float64)[cols].astype(np.float32)).cuda()
-        self.y = None if dual else torch.from_numpy(labels.astype(np.float32)).cuda()
+        self.y = None if dual else torch.from_numpy(labels.astype(np.float64)).cuda()
         d = self.d
         self.v = torch.zeros(d, dtype=torch.float64, device="cuda")
         self.u = torch.empty(d, dtype=torch.float32, device="cuda")

@@ -33,7 +33,7 @@ CASES = [
     (0, 0.05, dict(K=1, P=3, bucket_size=5, T3=2, T4=3, T1=4)),
     (0, 0.05, dict(K=1, P=2, bucket_size=4, sampling="iid", T3=2, T4=3, T1=4)),
     (0, 0.05, dict(K=1, P=5, bucket_size=1, T1=4)),
-    (0, 0.05, dict(K=1, P=2, bucket_size=25, T1=3)),
+    (0, 0.05, dict(K=1, P=2, bucket_size=12, T1=3)),  # partial last bucket
     (0, 0.05, dict(K=1, P=1, bucket_size=100, T1=3)),  # bucket larger than n (one bucket)
     # config 1 (svm dual), 2 (lasso), 3 (ridge), 4 (sparse logistic dual)
     (1, 0.0005, dict(K=1, P=8, bucket_size=4, T1=4)),
@@ -122,7 +122,7 @@ def test_degenerate_equals_sequential(cuda):
 
 def test_determinism_and_seed(cuda):
     from paper_1911_07722_b200 import SolverConfig, run_syscd
-    pb, _ = both(2, 0.02)
+    pb, _ = both(0, 0.05)
     cfg = SolverConfig(K=2, P=2, bucket_size=4, seed=11, T1=6)
     a, b = run_syscd(pb, cfg), run_syscd(pb, cfg)
     assert np.array_equal(a.alpha, b.alpha)
