@@ -128,10 +128,15 @@ typedef struct {
   float* partials;         /* device, [n_workers][part_ld] fp32, written here       */
   int64_t part_ld;
   int32_t* status;         /* device int, OR-ed with 2 on a non-finite step         */
+  void* workspace;         /* device scratch, >= syscd_dense_epoch_workspace_bytes   */
+  int64_t workspace_bytes;
 } syscd_dense_epoch_args;
 
 /* workers the dense epoch uses for this geometry (partials must hold that many rows) */
 int syscd_dense_epoch_workers(int64_t d, int32_t n_parts, int32_t* n_workers, int32_t* cluster);
+/* device scratch the epoch needs for this geometry (0 for the cluster kernel;
+ * the grid-wide kernel used for very tall columns needs its reduction slots) */
+int64_t syscd_dense_epoch_workspace_bytes(int64_t d, int32_t n_parts);
 int syscd_dense_epoch(const syscd_dense_epoch_args* e, void* stream);
 
 

@@ -36,7 +36,8 @@ class DenseEpochArgs(ctypes.Structure):
         ("kind", c_i32), ("d", c_i64), ("lda", c_i64), ("A", c_vp), ("sq", c_vp),
         ("alpha", c_vp), ("u", c_vp), ("seq", c_vp), ("work_prefix", c_vp), ("n_parts", c_i32),
         ("a", c_f64), ("lam", c_f64), ("n_coords", c_f64), ("iid", c_i32), ("n_store", c_i64),
-        ("partials", c_vp), ("part_ld", c_i64), ("status", c_vp),
+        ("partials", c_vp), ("part_ld", c_i64), ("status", c_vp), ("workspace", c_vp),
+        ("workspace_bytes", c_i64),
     ]
 
 
@@ -61,6 +62,7 @@ SIGNATURES = {
                            c_vp]),
     "syscd_dense_epoch_workers": (c_i32, [c_i64, c_i32, ctypes.POINTER(c_i32),
                                           ctypes.POINTER(c_i32)]),
+    "syscd_dense_epoch_workspace_bytes": (c_i64, [c_i64, c_i32]),
     "syscd_dense_epoch": (c_i32, [ctypes.POINTER(DenseEpochArgs), c_vp]),
     "syscd_sparse_epoch_workers": (c_i32, [c_i64, c_i32, ctypes.POINTER(c_i32)]),
     "syscd_sparse_epoch": (c_i32, [ctypes.POINTER(SparseEpochArgs), c_vp]),

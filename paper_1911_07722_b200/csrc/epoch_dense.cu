@@ -465,7 +465,13 @@ struct Choice {
   int G;
   int stages;
   size_t smem;
+  int grid;  // 1: grid-wide lookahead kernel (epoch_grid.cu)
 };
+
+int grid_choose(int64_t d, int* idx, int* G, int* stages, size_t* smem_out);
+int64_t grid_workspace_bytes(int G);
+int grid_launch(const syscd_dense_epoch_args* e, void* workspace, int64_t ws_bytes,
+                cudaStream_t stream);
 
 static int choose(int64_t d, int32_t n_parts, Choice* out) {
   std::lock_guard<std::mutex> lock(g_table_mu);
@@ -477,7 +483,7 @@ static int choose(int64_t d, int32_t n_parts, Choice* out) {
       cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const size_t budget = (size_t)smem_optin - 1024;
   double best = 1e300;
-  Choice bc = {-1, 0, 0, 0, 0};
+  Choice bc = {-1, 0, 0, 0, 0, 0};
   for (int i = 0; i < kTableSize; ++i) {
     KernelEntry& e = g_table[i];
     const int rows = entry_rows(e);
@@ -497,12 +503,21 @@ static int choose(int64_t d, int32_t n_parts, Choice* out) {
     const double t = std::max(lds + sync, hbm) / (double)G;
     if (t < best * 0.999) {
       best = t;
-      bc = {i, C, G, stages, smem};
+      bc = {i, C, G, stages, smem, 0};
     }
   }
+  // Grid-wide kernel: needed when no cluster holds the replica in registers,
+  // and preferred for tall columns when there are fewer partitions than
+  // clusters (one partition then streams over every SM instead of one GPC).
+  int gidx, gG, gst;
+  size_t gsm;
+  const bool grid_ok = grid_choose(d, &gidx, &gG, &gst, &gsm) == SYSCD_OK;
+  if (grid_ok && (bc.idx < 0 || (d >= 131072 && bc.G < 4 && n_parts < 4))) {
+    *out = {gidx, 1, 1, gst, gsm, 1};
+    return SYSCD_OK;
+  }
   if (bc.idx < 0) {
-    set_error("no dense epoch configuration covers d=%lld (max %d rows per cluster)",
-              (long long)d, 16 * 25920);
+    set_error("no dense epoch configuration covers d=%lld", (long long)d);
     return SYSCD_EINVAL;
   }
   *out = bc;
@@ -534,6 +549,16 @@ extern "C" int syscd_dense_epoch_workers(int64_t d, int32_t n_parts, int32_t* n_
   return SYSCD_OK;
 }
 
+extern "C" int64_t syscd_dense_epoch_workspace_bytes(int64_t d, int32_t n_parts) {
+  Choice ch;
+  if (d < 1 || n_parts < 1 || choose(d, n_parts, &ch) != SYSCD_OK) return -1;
+  if (!ch.grid) return 0;
+  int idx, G, st;
+  size_t sm;
+  grid_choose(d, &idx, &G, &st, &sm);
+  return grid_workspace_bytes(G);
+}
+
 extern "C" int syscd_dense_epoch(const syscd_dense_epoch_args* e, void* stream) {
   if (!e || !e->A || !e->sq || !e->alpha || !e->u || !e->seq || !e->work_prefix ||
       !e->partials || !e->status || e->d < 1 || e->n_parts < 1 || e->lda < e->d ||
@@ -552,6 +577,7 @@ extern "C" int syscd_dense_epoch(const syscd_dense_epoch_args* e, void* stream) 
     set_error("syscd_dense_epoch: part_ld < d");
     return SYSCD_EINVAL;
   }
+  if (ch.grid) return grid_launch(e, e->workspace, e->workspace_bytes, (cudaStream_t)stream);
   const KernelEntry& ke = g_table[ch.idx];
   DenseArgs args;
   args.A = e->A;

@@ -198,6 +198,8 @@ class _Engine:
             self.part_ld = (d + 31) // 32 * 32
             self.partials = torch.empty(self.n_workers * self.part_ld, dtype=torch.float32,
                                         device="cuda")
+            wsb = max(int(lib().syscd_dense_epoch_workspace_bytes(d, c)) for c in counts)
+            self.epoch_ws = torch.empty(max(wsb, 256), dtype=torch.uint8, device="cuda")
         else:
             nw = ctypes.c_int32(0)
             call("syscd_sparse_epoch_workers", d, self.n_parts_local, ctypes.byref(nw))
@@ -268,6 +270,8 @@ class _Engine:
             e.partials = self.partials.data_ptr()
             e.part_ld = self.part_ld
             e.status = self.status.data_ptr()
+            e.workspace = self.epoch_ws.data_ptr()
+            e.workspace_bytes = self.epoch_ws.numel()
             if self.kernel_events is not None:
                 self.kernel_events[0].record()
             call("syscd_dense_epoch", ctypes.byref(e), _stream())

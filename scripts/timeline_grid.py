@@ -1,0 +1,35 @@
+"""Per-event timeline of the grid-wide epoch kernel (CTA 0, first partition)."""
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from paper_1911_07722_b200._lib import lib
+from paper_1911_07722_b200.configs import workload
+from paper_1911_07722_b200.device import Dist
+from paper_1911_07722_b200.solvers import _Engine
+cfg_id = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+scale = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
+torch.cuda.set_device(0)
+wl = workload(cfg_id, scale=scale)
+eng = _Engine(wl.problem, wl.solver, Dist())
+eng.global_round(0)
+buf = torch.zeros(1024 * 8, dtype=torch.int64, device="cuda")
+L = lib(); L.syscd_debug_set_grid_timeline.argtypes = [ctypes.c_void_p]
+L.syscd_debug_set_grid_timeline(buf.data_ptr())
+eng.global_round(1)
+torch.cuda.synchronize()
+L.syscd_debug_set_grid_timeline(None)
+t = buf.view(1024, 8).cpu().numpy().astype(np.float64)
+t = t[100:900]
+ev = np.diff(t[:, 0])
+print(f"mean event {ev.mean():.0f} ns, median {np.median(ev):.0f}")
+print(f"  wait x staged   {np.mean(t[:,1]-t[:,0]):7.0f}")
+print(f"  partials+publish{np.mean(t[:,2]-t[:,1]):7.0f}")
+print(f"  wait totals     {np.mean(t[:,3]-t[:,2]):7.0f}")
+print(f"  resolve+axpy    {np.mean(t[:,4]-t[:,3]):7.0f}")
+print(f"  loop overhead   {np.mean(t[1:,0]-t[:-1,4]):7.0f}")
+# reducer: totals for pub r ready at t[r,5]; needed at event r+L (stamp 2)
+Lk = 3
+ready = t[:, 5]
+need = np.roll(t[:, 2], -Lk)
+print(f"  reducer interval {np.mean(np.diff(ready)):7.0f} ns; slack (need - ready) median {np.median((need-ready)[:-Lk]):7.0f}")
+print(f"  publish(r) -> totals(r) latency median {np.median(ready - t[:,2]):7.0f}")

@@ -40,3 +40,11 @@ def test_config0_full_size_verify(cuda):
     wl, res = _run(0, 20, verify=True)
     objs = [m.objective for m in res.metrics]
     assert all(b <= a for a, b in zip(objs, objs[1:]))
+
+
+def test_config3_ridge_full_size(cuda):
+    """1M x 8000 (32 GB) ridge on one GPU: grid-wide kernel, K=P=1."""
+    wl, res = _run(3, 2, verify=True)
+    objs = [m.objective for m in res.metrics]
+    assert objs[2] < objs[1] < objs[0]
+    assert all(m.updates == 8000 for m in res.metrics[1:])

@@ -42,6 +42,11 @@ CASES = [
     (2, 0.01, dict(K=1, P=1, bucket_size=8, T1=5)),
     (3, 0.002, dict(K=1, P=2, bucket_size=8, T1=4)),
     (4, 0.0002, dict(K=1, P=4, bucket_size=8, T1=4)),
+    # tall columns with few partitions -> grid-wide lookahead kernel
+    (3, 0.15, dict(K=1, P=1, bucket_size=8, T1=3)),
+    (3, 0.15, dict(K=1, P=2, bucket_size=8, T1=3)),
+    (2, 0.5, dict(K=1, P=1, bucket_size=8, T1=3)),
+    (2, 0.5, dict(K=1, P=3, bucket_size=4, T1=2)),
     (4, 0.0002, dict(K=2, P=3, bucket_size=16, sampling="iid", T3=3, T4=4, T1=3)),
 ]
 
