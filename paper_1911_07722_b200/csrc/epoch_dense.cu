@@ -469,6 +469,9 @@ struct Choice {
 };
 
 int grid_choose(int64_t d, int* idx, int* G, int* stages, size_t* smem_out);
+int small_workers(int32_t n_parts);
+int small_launch(const syscd_dense_epoch_args* e, cudaStream_t stream);
+constexpr int64_t kSmallMaxD = 32;
 int64_t grid_workspace_bytes(int G);
 int grid_launch(const syscd_dense_epoch_args* e, void* workspace, int64_t ws_bytes,
                 cudaStream_t stream);
@@ -541,6 +544,11 @@ extern "C" int syscd_dense_epoch_workers(int64_t d, int32_t n_parts, int32_t* n_
     set_error("syscd_dense_epoch_workers: invalid arguments");
     return SYSCD_EINVAL;
   }
+  if (d <= kSmallMaxD) {  // warp-per-partition chunked-Gram kernel (epoch_small.cu)
+    *n_workers = small_workers(n_parts);
+    if (cluster) *cluster = 0;
+    return SYSCD_OK;
+  }
   Choice ch;
   int st = choose(d, n_parts, &ch);
   if (st) return st;
@@ -550,6 +558,7 @@ extern "C" int syscd_dense_epoch_workers(int64_t d, int32_t n_parts, int32_t* n_
 }
 
 extern "C" int64_t syscd_dense_epoch_workspace_bytes(int64_t d, int32_t n_parts) {
+  if (d >= 1 && d <= kSmallMaxD && n_parts >= 1) return 0;
   Choice ch;
   if (d < 1 || n_parts < 1 || choose(d, n_parts, &ch) != SYSCD_OK) return -1;
   if (!ch.grid) return 0;
@@ -569,6 +578,13 @@ extern "C" int syscd_dense_epoch(const syscd_dense_epoch_args* e, void* stream) 
   if ((((uintptr_t)e->A) & 15) != 0) {
     set_error("syscd_dense_epoch: A must be 16-byte aligned");
     return SYSCD_EINVAL;
+  }
+  if (e->d <= kSmallMaxD) {
+    if (e->part_ld < e->d) {
+      set_error("syscd_dense_epoch: part_ld < d");
+      return SYSCD_EINVAL;
+    }
+    return small_launch(e, (cudaStream_t)stream);
   }
   Choice ch;
   int st = choose(e->d, e->n_parts, &ch);

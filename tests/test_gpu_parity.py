@@ -38,6 +38,8 @@ CASES = [
     # config 1 (svm dual), 2 (lasso), 3 (ridge), 4 (sparse logistic dual)
     (1, 0.0005, dict(K=1, P=8, bucket_size=4, T1=4)),
     (1, 0.0005, dict(K=2, P=4, bucket_size=32, T1=4)),
+    (1, 0.0005, dict(K=1, P=4, bucket_size=8, sampling="iid", T3=6, T4=8, T1=3)),
+    (1, 0.0002, dict(K=1, P=1, bucket_size=16, T1=4)),
     (2, 0.01, dict(K=1, P=4, bucket_size=2, T1=5)),
     (2, 0.01, dict(K=1, P=1, bucket_size=8, T1=5)),
     (3, 0.002, dict(K=1, P=2, bucket_size=8, T1=4)),
