@@ -169,14 +169,14 @@ def run_ours(args):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     start.record()
-    launches = 0
+    plans0 = eng.plans_issued
     for s in range(args.steps):
         t = args.warmup + s
-        if eng._ensure_plan(t) == 0 and eng.planned[0] == t:
-            launches += 3
         eng.kernel_events = (k_start[s], k_stop[s])
         eng.global_round(t)
-        launches += 3
+    # per round: epoch + reduce + apply (+ the per-round update-count copy is a
+    # cudaMemcpyAsync, not a kernel); per plan batch: 3 planning kernels
+    launches = 3 * args.steps + 3 * (eng.plans_issued - plans0)
     stop.record()
     torch.cuda.synchronize()
     if world > 1:

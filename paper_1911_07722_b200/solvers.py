@@ -185,10 +185,14 @@ class _Engine:
             call("syscd_plan_max_updates")
         self.R = max(1, min(cfg.plan_batch, cfg.n_rounds * cfg.T2 if cfg.n_rounds else 1))
         ws = int(L.syscd_plan_workspace_bytes(ctypes.byref(self.desc), self.R))
-        self.seq = torch.empty(self.R * max(1, self.stride), dtype=torch.int32, device="cuda")
-        self.wp = torch.empty(self.R * (self.n_parts_local + 1), dtype=torch.int64, device="cuda")
-        self.ws = torch.empty(max(ws, 256), dtype=torch.uint8, device="cuda")
-        self.planned = (None, None)  # [rid_lo, rid_hi)
+        # double-buffered round tables: batch b+1 is planned on a side stream
+        # while batch b's epochs run (the permutations are data-independent)
+        self.bufs = [_PlanBuf(torch, self.R, self.stride, self.n_parts_local, ws)
+                     for _ in range(2)]
+        self.cur = 0
+        self.side = torch.cuda.Stream()
+        self.upd_dev = torch.zeros(max(1, cfg.n_rounds * cfg.T2 + 1), dtype=torch.int64,
+                                   device="cuda")
         # workers
         d = dp.d
         if dp.storage == "dense":
@@ -214,6 +218,7 @@ class _Engine:
         self.dv = torch.empty(d, dtype=torch.float32, device="cuda")
         self.status = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.kernel_events = None  # (start, stop) CUDA events around the epoch kernel
+        self.plans_issued = 0      # syscd_plan calls (3 kernel launches each)
         self.launches = 0          # our kernel launches issued (bench accounting)
         dp.grad_into(self.v, self.u)
 
@@ -225,20 +230,38 @@ class _Engine:
         return nw.value, cl.value
 
     # -- one device round (rid) over node range [k0, k1) with lin_vec u -------
+    def _plan(self, buf, rid0, stream):
+        call("syscd_plan", ctypes.byref(self.desc), int(rid0), self.R, _ptr(buf.seq), self.stride,
+             _ptr(buf.wp), _ptr(buf.ws), buf.ws.numel(), ctypes.c_void_p(stream.cuda_stream))
+        buf.lo, buf.hi = rid0, rid0 + self.R
+        buf.ready.record(stream)
+        self.plans_issued += 1
+
     def _ensure_plan(self, rid):
-        lo, hi = self.planned
-        if lo is not None and lo <= rid < hi:
-            return rid - lo
-        n = self.R
-        call("syscd_plan", ctypes.byref(self.desc), int(rid), n, _ptr(self.seq), self.stride,
-             _ptr(self.wp), _ptr(self.ws), self.ws.numel(), _stream())
-        self.planned = (rid, rid + n)
-        return 0
+        """Buffer and row holding round rid's tables (rounds are consumed in
+        increasing order; the next batch is prefetched on the side stream)."""
+        torch = self.torch
+        cur = self.bufs[self.cur]
+        if cur.lo is not None and cur.lo <= rid < cur.hi:
+            return cur, rid - cur.lo
+        main = torch.cuda.current_stream()
+        nxt = self.bufs[1 - self.cur]
+        if nxt.lo is not None and nxt.lo <= rid < nxt.hi:
+            main.wait_event(nxt.ready)
+        else:
+            main.wait_event(nxt.free)
+            self._plan(nxt, rid, main)
+        cur.free.record(main)
+        self.cur = 1 - self.cur
+        # prefetch the following batch into the buffer just released
+        self.side.wait_event(cur.free)
+        self._plan(cur, nxt.hi, self.side)
+        return nxt, rid - nxt.lo
 
     def round_tables(self, rid):
-        r = self._ensure_plan(rid)
-        seq = self.seq[r * self.stride:]
-        wp = self.wp[r * (self.n_parts_local + 1):(r + 1) * (self.n_parts_local + 1)]
+        buf, r = self._ensure_plan(rid)
+        seq = buf.seq[r * self.stride:]
+        wp = buf.wp[r * (self.n_parts_local + 1):(r + 1) * (self.n_parts_local + 1)]
         return seq, wp
 
     def epoch(self, rid, u, node_lo=0, node_hi=None):
@@ -247,6 +270,12 @@ class _Engine:
         cfg, dp = self.cfg, self.dp
         node_hi = self.K_local if node_hi is None else node_hi
         seq, wp = self.round_tables(rid)
+        if node_lo == 0:
+            if rid >= self.upd_dev.numel():
+                grown = self.torch.zeros(2 * rid + 2, dtype=self.torch.int64, device="cuda")
+                grown[:self.upd_dev.numel()].copy_(self.upd_dev)
+                self.upd_dev = grown
+            self.upd_dev[rid:rid + 1].copy_(wp[self.n_parts_local:self.n_parts_local + 1])
         p0 = node_lo * cfg.P
         nparts = (node_hi - node_lo) * cfg.P
         wp_ptr = ctypes.c_void_p(wp.data_ptr() + 8 * p0)
@@ -339,8 +368,7 @@ class _Engine:
         dp.grad_into(self.v, self.u)
 
     def updates_last_round(self, rid):
-        _, wp = self.round_tables(rid)
-        return int(wp[self.n_parts_local].item())
+        return int(self.upd_dev[rid].item())
 
     def check_status(self):
         st = int(self.status.item())
@@ -350,6 +378,7 @@ class _Engine:
 
     def census_ok(self, rid):
         seq, wp = self.round_tables(rid)
+        self.torch.cuda.synchronize()
         tot = int(wp[self.n_parts_local].item())
         s = seq[:tot]
         return int(torch_unique_count(s)) == tot
@@ -364,6 +393,17 @@ class _Engine:
         full[torch.from_numpy(dp.store_cols).cuda()] = self.alpha.double()
         self.dist.allreduce_(full)
         return full.cpu().numpy()
+
+
+class _PlanBuf:
+    def __init__(self, torch, R, stride, n_parts, ws_bytes):
+        self.seq = torch.empty(R * max(1, stride), dtype=torch.int32, device="cuda")
+        self.wp = torch.empty(R * (n_parts + 1), dtype=torch.int64, device="cuda")
+        self.ws = torch.empty(max(ws_bytes, 256), dtype=torch.uint8, device="cuda")
+        self.lo = self.hi = None
+        self.ready = torch.cuda.Event()
+        self.free = torch.cuda.Event()
+        self.free.record()
 
 
 def torch_unique_count(t):
