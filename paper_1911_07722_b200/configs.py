@@ -171,13 +171,70 @@ def host_problem(cfg_id, scale=1.0, seed=0):
 # ---------------------------------------------------------------------------
 # device (torch) generation for full-size runs
 # ---------------------------------------------------------------------------
+def _device_onehot_rows(n, d, nnz_row, gen, chunk=1 << 20):
+    """n rows of nnz_row distinct features drawn from Zipf(1.1) over d
+    features (inverse-CDF draws, first nnz_row distinct in draw order),
+    returned sorted per row as an (n, nnz_row) int32 CUDA tensor."""
+    import torch
+    ranks = torch.arange(1, d + 1, dtype=torch.float64, device="cuda")
+    cdf = torch.cumsum(ranks.pow(-1.1), 0)
+    cdf /= cdf[-1].clone()
+    out = torch.empty((n, nnz_row), dtype=torch.int32, device="cuda")
+    ncand = 4 * nnz_row
+    for r0 in range(0, n, chunk):
+        rows = torch.arange(r0, min(n, r0 + chunk), device="cuda")
+        while rows.numel():
+            R = rows.numel()
+            u = torch.rand((R, ncand), generator=gen, device="cuda", dtype=torch.float64)
+            cand = torch.searchsorted(cdf, u).clamp_(max=d - 1)
+            sv, pos = torch.sort(cand, dim=1, stable=True)
+            first = torch.ones_like(sv, dtype=torch.bool)
+            first[:, 1:] = sv[:, 1:] != sv[:, :-1]
+            keep = torch.zeros_like(first)
+            keep.scatter_(1, pos, first)                 # first occurrence, draw order
+            rank = torch.cumsum(keep.to(torch.int32), 1)
+            ok = rank[:, -1] >= nnz_row
+            sel = keep & (rank <= nnz_row)
+            good = rows[ok]
+            feats = cand[ok][sel[ok]].view(-1, nnz_row)
+            out[good] = torch.sort(feats, dim=1).values.to(torch.int32)
+            rows = rows[~ok]
+    return out
+
+
+def _device_config4(d, n, seed, gen):
+    import torch
+    nnz_row = 39 if d >= 390 else max(1, d // 10)
+    feats = _device_onehot_rows(n, d, nnz_row, gen)
+    w = torch.zeros(d, dtype=torch.float64, device="cuda")
+    k = max(1, d // 100)
+    idx = torch.randperm(d, generator=gen, device="cuda")[:k]
+    w[idx] = 3.0 * torch.randn(k, generator=gen, device="cuda", dtype=torch.float64)
+    score = w[feats.long()].sum(dim=1)
+    lo, hi = float(score.min()) - 20.0, float(score.max()) + 20.0
+    for _ in range(60):  # bias so that the expected positive rate is 25%
+        mid = 0.5 * (lo + hi)
+        if float(torch.sigmoid(score - mid).mean()) > 0.25:
+            lo = mid
+        else:
+            hi = mid
+    prob = torch.sigmoid(score - 0.5 * (lo + hi))
+    y = torch.where(torch.rand(n, generator=gen, device="cuda", dtype=torch.float64) < prob,
+                    1.0, -1.0)
+    col_ptr = torch.arange(0, (n + 1) * nnz_row, nnz_row, dtype=torch.int64, device="cuda")
+    vals = torch.ones(n * nnz_row, dtype=torch.float32, device="cuda")
+    m = ColumnMatrix.from_device_csc(col_ptr, feats.reshape(-1).contiguous(), vals, d)
+    ds = LabeledDataset(m, y.cpu().numpy(), COORDINATES_ARE_EXAMPLES)
+    return GlmProblem.build(ds, SmoothLoss.logistic(), 1e-6)
+
+
 def device_problem(cfg_id, scale=1.0, seed=0):
     import torch
     d, n = _dims(cfg_id, scale)
     gen = torch.Generator(device="cuda")
     gen.manual_seed(1_000_003 * (seed + 1) + cfg_id)
     if cfg_id == 4:
-        return host_problem(4, scale, seed)  # sparse generator stays on the host
+        return _device_config4(d, n, seed, gen)
     ld = padded_ld(d)
     At = torch.empty((n, ld), dtype=torch.float32, device="cuda")
     chunk = max(1, (1 << 28) // ld)
@@ -231,7 +288,7 @@ def device_problem(cfg_id, scale=1.0, seed=0):
 
 def workload(cfg_id, scale=1.0, seed=0, host=None, n_gpus=1, epochs=None):
     if host is None:
-        host = cfg_id in (0, 4) or scale < 0.2
+        host = cfg_id == 0 or (scale < 0.2 and cfg_id != 4) or (cfg_id == 4 and scale < 0.002)
     pb = host_problem(cfg_id, scale, seed) if host else device_problem(cfg_id, scale, seed)
     solver = default_solver(cfg_id, n_gpus, epochs)
     m = pb.data.matrix

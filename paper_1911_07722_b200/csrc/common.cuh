@@ -21,23 +21,32 @@ __device__ __forceinline__ double sigmoid_d(double s) {
   return e / (1.0 + e);
 }
 
+// fp32 logistic with SFU exp (relative error ~1e-7, below alpha's fp32 storage)
+__device__ __forceinline__ double sigmoid_fast(double s) {
+  const float e = __expf(-fabsf((float)s));
+  const float r = __fdividef(1.f, 1.f + e);
+  return (double)(s >= 0.0 ? r : e * r);
+}
+
 // Root of h(s) = lin + aq (sigma(s) - alpha) + s/n in log-odds s (the oracle's
-// logistic_dual_newton, oracle/objectives.py): bracketed Newton + bisection.
+// logistic_dual_newton, oracle/objectives.py): bracketed Newton + bisection in
+// fp64, with the sigmoid / logit evaluated by fp32 SFU intrinsics.  The result
+// is stored as fp32 alpha = sigma(s) and sigma' <= 1/4, so the iteration stops
+// at |ds| <= 1e-9 max(1,|s|) (the oracle uses 1e-13 with fp64 transcendentals).
 __device__ __forceinline__ double logistic_dual_solve(double lin, double aq, double alpha,
                                                       double n) {
   const double inv_n = 1.0 / n;
   double lo = -n * (lin + aq * (1.0 - alpha)) - 1.0;
   double hi = n * (aq * alpha - lin) + 1.0;
-  double s;
+  double s = 0.0;
   if (alpha > 0.0 && alpha < 1.0) {
-    s = log(alpha) - log1p(-alpha);
-  } else {
-    s = 0.0;
+    const float af = (float)alpha;
+    s = (double)(__logf(af) - __logf(1.f - af));
   }
   s = fmin(fmax(s, lo), hi);
   for (int it = 0; it < 100; ++it) {
-    double t = sigmoid_d(s);
-    double h = lin + aq * (t - alpha) + s * inv_n;
+    const double t = sigmoid_fast(s);
+    const double h = lin + aq * (t - alpha) + s * inv_n;
     if (h > 0.0) {
       hi = s;
     } else if (h < 0.0) {
@@ -45,14 +54,14 @@ __device__ __forceinline__ double logistic_dual_solve(double lin, double aq, dou
     } else {
       break;
     }
-    double dh = aq * t * (1.0 - t) + inv_n;
+    const double dh = aq * t * (1.0 - t) + inv_n;
     double ns = s - h / dh;
     if (!(lo < ns && ns < hi)) ns = 0.5 * (lo + hi);
-    double step = ns - s;
+    const double step = ns - s;
     s = ns;
-    if (fabs(step) <= 1e-13 * fmax(1.0, fabs(s))) break;
+    if (fabs(step) <= 1e-9 * fmax(1.0, fabs(s))) break;
   }
-  return sigmoid_d(s);
+  return sigmoid_fast(s);
 }
 
 __device__ __forceinline__ double coord_step(int kind, double lin, double a, double q, double lam,

@@ -7,8 +7,8 @@
 // private replica dv of the running partition is a dense fp32 d-vector in
 // HBM/L2 that is all-zero between partitions: only the rows the partition's
 // columns touch are ever non-zero, and the flush re-walks those columns,
-// adds each touched entry once into the node sum `delta_v` (red.global.add)
-// and zeroes it again.  Work and traffic are therefore proportional to nnz,
+// zeroes it again; every update also adds delta*x_j into the node sum
+// `delta_v` with a fire-and-forget red.global.add.  Work and traffic are therefore proportional to nnz,
 // never to workers x d.  Per update, lanes own nonzeros: gather u[i] and
 // dv[i], warp-reduce x.(u + a dv), fp64 step, scatter dv[i] += delta x_i
 // (rows of one column are distinct, so the scatter is conflict-free).
@@ -34,6 +34,7 @@ struct SparseArgs {
   const int64_t* wp;
   int32_t n_parts;
   float a;
+  float lam_f, inv_n_f;
   double a_d, lam, n_coords;
   int32_t kind, iid;
   float* dv_work;
@@ -66,45 +67,78 @@ __global__ void __launch_bounds__(256) k_sparse_epoch(SparseArgs A) {
   float* dv = A.dv_work + (int64_t)g * A.d;
   for (int64_t p = p_lo; p < p_hi; ++p) {
     const int64_t s0 = A.wp[p], s1 = A.wp[p + 1];
+    if (s1 == s0) continue;
+    // software pipeline: the next update's column (<= 32 nonzeros per lane
+    // pass) and scalars are loaded while the current one is processed
+    int jn = A.seq[s0];
+    int64_t en0 = A.cp[jn], en1 = A.cp[jn + 1];
+    int rn = en0 + lane < en1 ? A.ri[en0 + lane] : 0;
+    float vn = en0 + lane < en1 ? A.vals[en0 + lane] : 0.f;
+    float an = A.iid ? 0.f : A.alpha[jn];
+    float qn = __ldg(A.sq + jn);
     for (int64_t s = s0; s < s1; ++s) {
-      const int j = A.seq[s];
-      const int64_t e0 = A.cp[j], e1 = A.cp[j + 1];
+      const int j = jn;
+      const int64_t e0 = en0, e1 = en1;
+      const int r_first = rn;
+      const float v_first = vn;
+      float aj = an;
+      const float qj = qn;
+      if (s + 1 < s1) {
+        jn = A.seq[s + 1];
+        en0 = A.cp[jn];
+        en1 = A.cp[jn + 1];
+        rn = en0 + lane < en1 ? A.ri[en0 + lane] : 0;
+        vn = en0 + lane < en1 ? A.vals[en0 + lane] : 0.f;
+        if (!A.iid) an = A.alpha[jn];
+        qn = __ldg(A.sq + jn);
+      }
       float acc = 0.f;
-      for (int64_t e = e0 + lane; e < e1; e += 32) {
+      if (e0 + lane < e1) acc = v_first * fmaf(A.a, dv[r_first], A.u[r_first]);
+      for (int64_t e = e0 + 32 + lane; e < e1; e += 32) {
         const int i = A.ri[e];
         acc = fmaf(A.vals[e], fmaf(A.a, dv[i], A.u[i]), acc);
       }
       acc = warp_sum(acc);
-      const float aj = A.iid ? *(volatile float*)(A.alpha + j) : A.alpha[j];
-      const double anew =
-          coord_step(A.kind, (double)acc, A.a_d, (double)A.sq[j], A.lam, (double)aj, A.n_coords);
+      if (A.iid) aj = *(volatile float*)(A.alpha + j);
+      float anew;
+      if (A.kind == SYSCD_LOGISTIC_DUAL) {
+        anew = (float)coord_step(A.kind, (double)acc, A.a_d, (double)qj, A.lam, (double)aj,
+                                 A.n_coords);
+      } else {
+        anew = coord_step_f(A.kind, acc, A.a, qj, A.lam_f, aj, A.inv_n_f);
+      }
       float delta = 0.f;
       if (isfinite(anew)) {
-        const float an = (float)anew;
-        delta = an - aj;
-        if (lane == 0) A.alpha[j] = an;
+        delta = anew - aj;
+        if (lane == 0) A.alpha[j] = anew;
       } else if (lane == 0) {
         atomicOr(A.status, SYSCD_ENONFINITE);
       }
-      for (int64_t e = e0 + lane; e < e1; e += 32) {
-        const int i = A.ri[e];
-        dv[i] = fmaf(delta, A.vals[e], dv[i]);
-      }
-      __syncwarp();
-    }
-    // flush: every touched row once into delta_v, then back to zero
-    for (int64_t s = s0; s < s1; ++s) {
-      const int j = A.seq[s];
-      for (int64_t e = A.cp[j] + lane; e < A.cp[j + 1]; e += 32) {
-        const int i = A.ri[e];
-        const float val = dv[i];
-        if (val != 0.f) {
-          atomicAdd(A.delta_v + i, val);
-          dv[i] = 0.f;
+      // private replica for the partition's own dots, plus a fire-and-forget
+      // contribution to the node sum (no end-of-partition gather pass)
+      if (delta != 0.f) {
+        if (e0 + lane < e1) {
+          const float c = delta * v_first;
+          dv[r_first] += c;
+          red_add_f32(A.delta_v + r_first, c);
+        }
+        for (int64_t e = e0 + 32 + lane; e < e1; e += 32) {
+          const int i = A.ri[e];
+          const float c = delta * A.vals[e];
+          dv[i] += c;
+          red_add_f32(A.delta_v + i, c);
         }
       }
       __syncwarp();
     }
+    // restore the all-zero replica: lanes walk different columns in parallel
+    // (a row shared by two columns is simply zeroed twice)
+    for (int64_t s = s0 + lane; s < s1; s += 32) {
+      const int j = A.seq[s];
+      const int64_t c0 = A.cp[j], c1 = A.cp[j + 1];
+      for (int64_t e = c0; e < c1; ++e) dv[A.ri[e]] = 0.f;
+    }
+    __syncwarp();
   }
 }
 
@@ -150,6 +184,8 @@ extern "C" int syscd_sparse_epoch(const syscd_sparse_epoch_args* e, void* stream
   A.n_parts = e->n_parts;
   A.a = (float)e->a;
   A.a_d = e->a;
+  A.lam_f = (float)e->lam;
+  A.inv_n_f = (float)(1.0 / e->n_coords);
   A.lam = e->lam;
   A.n_coords = e->n_coords;
   A.kind = e->kind;

@@ -181,19 +181,25 @@ class DeviceProblem:
             self.mdev = ("dense", self.At)
         else:
             cp, ri, va = device_csc(m)
-            if not natural or dual:
-                cp_h = cp.cpu().numpy()
-                cnt = cp_h[cols + 1] - cp_h[cols]
-                new_cp = np.zeros(cols.size + 1, dtype=np.int64)
-                np.cumsum(cnt, out=new_cp[1:])
-                src = np.concatenate([np.arange(cp_h[c], cp_h[c + 1]) for c in cols]) if cols.size else np.zeros(0, np.int64)
-                src_t = torch.from_numpy(src).cuda()
-                ri2 = ri.index_select(0, src_t)
-                va2 = va.index_select(0, src_t)
-                if dual:
-                    ycol = np.repeat(labels[cols], cnt).astype(np.float32)
-                    va2 = va2 * torch.from_numpy(ycol).cuda()
-                cp, ri, va = torch.from_numpy(new_cp).cuda(), ri2.contiguous(), va2.contiguous()
+            if not natural:
+                # gather the shard's columns (vectorised on the device)
+                cols_d = torch.from_numpy(cols).cuda()
+                starts = cp.index_select(0, cols_d)
+                cnt = cp.index_select(0, cols_d + 1) - starts
+                new_cp = torch.zeros(cols.size + 1, dtype=torch.int64, device="cuda")
+                torch.cumsum(cnt, 0, out=new_cp[1:])
+                nnz = int(new_cp[-1])
+                rep = torch.repeat_interleave(torch.arange(cols.size, device="cuda"), cnt,
+                                              output_size=nnz)
+                src = starts.index_select(0, rep) + (torch.arange(nnz, device="cuda") -
+                                                     new_cp.index_select(0, rep))
+                cp, ri, va = new_cp, ri.index_select(0, src), va.index_select(0, src)
+            if dual:
+                # fold labels into the values: column i becomes y_i x_i
+                cnt = cp[1:] - cp[:-1]
+                ycol = torch.from_numpy(labels[cols].astype(np.float32)).cuda()
+                va = va * torch.repeat_interleave(ycol, cnt, output_size=int(cp[-1]))
+            cp, ri, va = cp.contiguous(), ri.contiguous(), va.contiguous()
             self.csc = (cp, ri, va)
             self.mdev = ("sparse", self.csc)
             self.lda = None
