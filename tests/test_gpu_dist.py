@@ -1,0 +1,70 @@
+"""The sharded multi-GPU engine path, run as two ranks that share the one GPU
+of the test box with the gloo backend (host-staged all-reduce; no kernel
+waits on another rank).  Each rank owns K/2 node groups and gathers their
+buckets' columns; per round the ranks all-reduce dv (solvers.py:423).  The
+result must match the oracle run with the same K."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank(rank, world, port, cfg_id, scale, kw, q):
+    import torch
+    import torch.distributed as tdist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1911_07722_b200 import SolverConfig, run_syscd
+        from paper_1911_07722_b200.configs import host_problem
+        pb = host_problem(cfg_id, scale, 0)
+        res = run_syscd(pb, SolverConfig(seed=0, compute_gap=True, **kw))
+        q.put((rank, res.alpha.tolist(), [m.objective for m in res.metrics],
+               [m.gap for m in res.metrics], [m.updates for m in res.metrics]))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg_id,scale,kw", [
+    (0, 0.05, dict(K=2, P=2, bucket_size=4, T1=5)),
+    (2, 0.01, dict(K=2, P=1, bucket_size=2, T1=4)),
+    (1, 0.0005, dict(K=4, P=2, bucket_size=8, T1=3)),
+    (4, 0.0002, dict(K=2, P=2, bucket_size=8, T1=3)),
+    (0, 0.05, dict(K=2, P=2, bucket_size=4, T2=2, T1=3)),
+])
+def test_two_rank_parity(cuda, cfg_id, scale, kw):
+    from gpu_helpers import oracle_problem
+    from oracle import syscd_oracle as O
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rank, args=(r, world, port, cfg_id, scale, kw, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    (_, a0, o0, g0, u0), (_, a1, o1, g1, u1) = out
+    assert a0 == a1 and o0 == o1 and u0 == u1      # ranks agree exactly
+    ores = O.run_syscd(oracle_problem(cfg_id, scale), O.OracleConfig(seed=0, with_gap=True, **kw))
+    ref = np.array([r.objective for r in ores.rows])
+    floor = 1e-6 * max(abs(ref[0]), 1e-12)
+    assert np.max(np.abs(np.array(o0) - ref) / np.maximum(np.abs(ref), floor)) < 1e-4
+    assert u0 == [r.updates for r in ores.rows]
+    na = np.linalg.norm(ores.alpha)
+    assert np.linalg.norm(np.array(a0) - ores.alpha) / na < 1e-3
