@@ -97,23 +97,26 @@ __device__ __forceinline__ float coord_step_f(int kind, float lin, float a, floa
   switch (kind) {
     case SYSCD_RIDGE:
     case SYSCD_LOGISTIC:
-      return alpha - __fdiv_rn(lin + lam * alpha, aq + lam);
+      return alpha - (lin + lam * alpha) * __frcp_rn(aq + lam);
     case SYSCD_LASSO: {
       if (aq <= 0.f) return 0.f;
-      const float z = alpha - __fdiv_rn(lin, aq);
-      const float m = fabsf(z) - __fdiv_rn(lam, aq);
+      const float r = __frcp_rn(aq);
+      const float z = fmaf(-lin, r, alpha);
+      const float m = fmaf(-lam, r, fabsf(z));
       return m > 0.f ? copysignf(m, z) : 0.f;
     }
     default: {  // SVM dual
       if (aq <= 0.f) return 1.f;
-      const float z = alpha - __fdiv_rn(lin - inv_n, aq);
+      const float z = fmaf(-(lin - inv_n), __frcp_rn(aq), alpha);
       return fminf(fmaxf(z, 0.f), 1.f);
     }
   }
 }
 
+// fire-and-forget fp32 add; no "memory" clobber so independent loads (e.g.
+// read-only u in the partition flush) may be scheduled across it
 __device__ __forceinline__ void red_add_f32(float* p, float v) {
-  asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+  asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v));
 }
 
 // ---------------------------------------------------------------------------
