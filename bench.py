@@ -127,8 +127,6 @@ def f_star_for(problem, cfg_id, epochs=200):
     solved with K=P=1 (exact updates, a = gamma) until the relative model
     change stalls; returns (F*, gap at F*)."""
     from paper_1911_07722_b200 import SolverConfig, run_syscd
-    if cfg_id in (1, 4):
-        return None, None
     B = 8
     cfg = SolverConfig(K=1, P=1, bucket_size=B, T1=None, max_epochs=epochs, tolerance=1e-7,
                        metrics_every=10_000, compute_gap=True, seed=1)
@@ -258,13 +256,46 @@ def run_ours(args):
 
 
 def time_to_target(wl, args, target=1e-4, max_epochs=2000):
+    """Epochs and summed epoch seconds until the target accuracy.
+
+    Primal (ridge / lasso): relative suboptimality (F - F*)/(F0 - F*) with F*
+    from a K=P=1 GPU solve of the same problem (test_acceptance.py:77-87).
+    Dual (svm / logistic): relative duality gap gap/|P(w)|, a certificate that
+    needs no F* (SURVEY 8(d)); the run is capped, and the best value reached is
+    reported when the target is not hit.
+    """
     import dataclasses
     from paper_1911_07722_b200 import run_syscd
     pb = wl.problem
-    if wl.cfg_id in (1, 4):
-        return {"note": "dual objective: suboptimality via duality gap not yet reported"}
+    dual = pb.is_dual
+    if dual:
+        cap = {1: 300, 4: 60}.get(wl.cfg_id, 200)
+        cfg = dataclasses.replace(wl.solver, T1=cap, metrics_every=max(1, cap // 30),
+                                  compute_gap=True)
+        res = run_syscd(pb, cfg)
+        t, hit, best, secs = 0.0, None, None, []
+        for m in res.metrics[1:]:
+            secs.append(m.seconds)
+        # metrics rows are every k epochs; seconds of skipped epochs are not in
+        # the rows, so accumulate from the engine's per-row seconds scaled by k
+        k = cfg.metrics_every
+        for m in res.metrics[1:]:
+            t += m.seconds * k
+            primal = m.gap - m.objective  # gap = P(w) + F
+            rel = m.gap / max(abs(primal), 1e-300)
+            best = rel if best is None else min(best, rel)
+            if hit is None and rel <= target:
+                hit = {"epoch": m.epoch, "seconds": t}
+        return {"target": target, "definition": "duality gap / |P(w)| (dual objective)",
+                "hit": hit, "best_rel_gap": best, "epochs_run": res.metrics[-1].epoch,
+                "epoch_seconds_total_est": t,
+                "rel_gap_at_config_epochs": next((m.gap / max(abs(m.gap - m.objective), 1e-300)
+                                                  for m in res.metrics
+                                                  if m.epoch >= wl.solver.T1), None),
+                "config_epochs": wl.solver.T1}
     f_star, gap_star = f_star_for(pb, wl.cfg_id)
-    cfg = dataclasses.replace(wl.solver, T1=max_epochs, metrics_every=1, compute_gap=False)
+    cfg = dataclasses.replace(wl.solver, T1=max_epochs if wl.cfg_id != 3 else 200,
+                              metrics_every=1, compute_gap=False)
     res = run_syscd(pb, cfg, f_star=f_star)
     f0 = res.metrics[0].objective
     t = 0.0
@@ -313,7 +344,7 @@ def e2e_run(args, wl, world, dist):
         dev = host.to("cuda", non_blocking=True)
         mm = ColumnMatrix.from_device(dev, m.n_rows)
         ds = LabeledDataset(mm, labels, pb.data.orientation)
-        p2 = GlmProblem(ds, pb.loss, pb.reg, pb.stats)
+        p2 = GlmProblem.build(ds, pb.loss, pb.reg.lam, reg=pb.reg.kind)
         res = run_syscd(p2, cfg)
         _ = res.alpha.sum()
         torch.cuda.synchronize()
@@ -327,8 +358,8 @@ def e2e_run(args, wl, world, dist):
     return {"value": upd / float(tt), "unit": "updates/s",
             "h2d_bytes_per_step": int(host.numel() * 4 + labels.size * 8),
             "d2h_bytes_per_step": int(m.n_cols * 8),
-            "step": f"run_syscd over {cfg.T1} epochs on a host-resident problem "
-                    "(pinned H2D of A and y, fresh device state, alpha D2H)",
+            "step": f"GlmProblem.build + run_syscd over {cfg.T1} epochs on a host-resident "
+                    "problem (pinned H2D of A and y, column norms, fresh device state, alpha D2H)",
             "seconds_per_step": float(tt) / len(times)}
 
 
