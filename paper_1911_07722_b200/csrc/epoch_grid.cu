@@ -7,24 +7,29 @@
 // a time; CTA c owns rows [c*CTA_ROWS, (c+1)*CTA_ROWS) and every coordinate's
 // dot product is reduced across the grid through global memory.
 //
-// Latency hiding (s-step lookahead, exact in real arithmetic): when column e
-// of a partition is staged, the latest applied update is e-L-1, so each CTA
-// computes
-//     s_e = x_e . w_{<= e-L-1}   and   g_{e,k} = x_e . x_{e-k},  k = 1..L
-// publishes these L+1 partials, and resolves column e-L with
-//     lin_{e-L} = S_{e-L} + a * sum_k delta_{e-L-k} G_{e-L,k}
-// from grid totals published L events earlier (exact: w_{<=e-2L-1} plus the
-// L updates e-2L..e-L-1 accounted through the cross terms).  The last L+1
-// columns live in a register ring, so the cross terms cost FMAs only.
+// Blocked lookahead (exact in real arithmetic).  Columns are taken BB at a
+// time ("blocks"); when block e is staged, the updates of blocks <= e-LL-1 are
+// already applied to w, and each CTA publishes, for its rows,
+//     s_i      = x_{e,i} . w                      i < BB
+//     gin(i,k) = x_{e,i} . x_{e,k}                k < i       (in-block Gram)
+//     gx(l,i,k)= x_{e,i} . x_{e-l,k}              l = 1..LL   (cross-block Gram)
+// Block e-LL is then resolved from the grid totals one column at a time:
+//     lin_i = S_i + a sum_{l,k} delta_{e-LL-l,k} GX(l,i,k) + a sum_{k<i} delta_{e-LL,k} GIN(i,k)
+// and w += a sum_i delta_i x_{e-LL,i}.  The last LL+1 blocks live in a
+// register ring, so every Gram term is an FMA.  BB amortises the per-event
+// synchronisation (CTA reduction, publication, grid gather) over BB columns;
+// LL hides the grid-reduction latency behind LL events.
 //
-// Warp roles per CTA: 1 TMA producer warp (column slices into a shared-memory
-// ring + (j, alpha_j, q_j) metadata ring), 1 reducer warp (waits on the grid
-// counter of each published step, sums the G partial records in a fixed order
-// and hands the totals to the math warps through an mbarrier), NTC/32 math
-// warps.  Totals are summed in the same order in every CTA, so all CTAs take
-// bit-identical steps and the result is deterministic.  Partitions run one
-// after another; between them the pipeline drains, (w-u)/a is folded into
-// `out` (each row has exactly one writer) and w is reset to u.
+// Partials are published as 64-bit words (tag << 32 | float bits), one word
+// per value, component-major: the word is single-copy atomic, so a reader that
+// sees the expected tag also sees the value -- no counter, fence or acquire
+// round trip.  Two reducer warps gather alternate events (each lane loads its
+// CTAs' words of every component at once, warp vote on the tags), sum the G
+// records in a fixed order and hand the totals to the math warps through an
+// mbarrier.  Every CTA sums identically, so all CTAs take bit-identical steps
+// and the result is deterministic.  Partitions run one after another; at a
+// partition end the pipeline drains, (w-u)/a is folded into `out` (each row
+// has exactly one writer) and w is reset to u.
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -35,10 +40,10 @@
 
 namespace syscd {
 
-constexpr int kGNB = 16;    // global partial-record slots (> 2L+1)
-constexpr int kGMeta = 64;  // metadata ring (steps)
-constexpr int kGTot = 8;    // totals ring in shared memory (> L)
-constexpr int kGRec = 8;    // floats per partial record (L+1 <= 8)
+constexpr int kGNB = 16;    // global record slots (events), > 2*LL+2
+constexpr int kGMeta = 64;  // metadata ring (columns)
+constexpr int kGTot = 8;    // totals ring in shared memory (events), > LL+1
+constexpr int kGVal = 32;   // max values per event record
 
 struct GridArgs {
   const float* A;
@@ -57,10 +62,10 @@ struct GridArgs {
   int32_t kind;
   int32_t stages;
   int32_t evict_first;
-  float* out;                   // [d] summed replicas (one worker row)
-  unsigned long long* recs;     // [kGNB][G][kGRec] tagged partials, zeroed before launch
+  float* out;                // [d] summed replicas (one worker row)
+  unsigned long long* recs;  // [kGNB][NS][G] tagged partials, zeroed before launch
   int32_t* status;
-  unsigned long long* dbg;      // optional timeline (CTA 0)
+  unsigned long long* dbg;   // optional timeline (CTA 0)
 };
 
 __device__ __forceinline__ unsigned long long gtimer_g() {
@@ -87,9 +92,9 @@ __host__ __device__ inline GridSmem grid_smem(int stages, int cta_rows) {
   o += kGTot * 8;
   o = galign(o, 16);
   L.tot = o;
-  o += kGTot * kGRec * 4;
+  o += kGTot * kGVal * 4;
   L.red = o;
-  o += 2 * 32 * kGRec * 4;
+  o += 2 * 16 * kGVal * 4;
   o = galign(o, 16);
   L.meta = o;
   o += kGMeta * 16;
@@ -97,27 +102,38 @@ __host__ __device__ inline GridSmem grid_smem(int stages, int cta_rows) {
   return L;
 }
 
-// A partial is published as one 64-bit word (tag << 32 | float bits): the
-// word is single-copy atomic, so a reader that sees the expected tag also
-// sees the value -- no counter, fence or acquire round trip is needed.
+// A partial is one 64-bit word (tag << 32 | float bits).
 __device__ __forceinline__ void st_tagged(unsigned long long* p, uint32_t tag, float v) {
   const unsigned long long w = ((unsigned long long)tag << 32) | __float_as_uint(v);
   asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
 }
 
-__device__ __forceinline__ void ld_tagged2(const unsigned long long* p, unsigned long long& a,
-                                           unsigned long long& b) {
-  asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];"
-               : "=l"(a), "=l"(b)
-               : "l"(p)
-               : "memory");
+__device__ __forceinline__ unsigned long long ld_tagged(const unsigned long long* p) {
+  unsigned long long w;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+  return w;
 }
 
-template <int RR, int L>
+template <int BB, int LL>
+struct GridLayout {
+  static constexpr int kS = 0;
+  static constexpr int kIn = BB;
+  static constexpr int kX = BB + BB * (BB - 1) / 2;
+  static constexpr int kNS = kX + LL * BB * BB;
+  __host__ __device__ static constexpr int gin(int i, int k) { return kIn + i * (i - 1) / 2 + k; }
+  __host__ __device__ static constexpr int gx(int l, int i, int k) {
+    return kX + ((l - 1) * BB + i) * BB + k;
+  }
+};
+
+template <int RR, int BB, int LL>
 __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
   constexpr int NTC = 416;  // 13 math warps + producer + 2 reducers = 16 warps
   constexpr int NWC = NTC / 32;
-  constexpr int NS = L + 1;
+  constexpr int NSLOT = LL + 1;
+  using Lay = GridLayout<BB, LL>;
+  constexpr int NS = Lay::kNS;
+  static_assert(NS <= kGVal, "event record too large");
   constexpr int CTA_ROWS = NTC * RR;
 
   extern __shared__ __align__(128) unsigned char smem[];
@@ -189,55 +205,42 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
     }
   } else if (warp > NWC) {
     // ---------------------------------------------------------------- reducers
-    // Two warps take alternate published steps.  For step r every lane issues
-    // the 16-byte loads of all its CTAs' records at once (CTAs c = lane +
-    // 32q), checks the tags with a warp vote and re-polls until the step is
-    // complete; then each lane sums its CTAs in order and the warp folds the
-    // lanes with a fixed butterfly -- identical totals in every CTA.
-    constexpr int NV = (NS + 1) / 2;  // 16-byte loads per record
-    constexpr int NQ = 5;             // ceil(148 / 32) records per lane
-    const int64_t pubs = s_end - s_begin;
-    for (int64_t r = warp - NWC - 1; r < pubs; r += 2) {
-      const unsigned long long* rec = A.recs + (size_t)(r % kGNB) * G * kGRec;
+    constexpr int NQ = 5;  // ceil(148 / 32) CTAs per lane
+    int64_t events = 0;
+    for (int p = 0; p < A.n_parts; ++p) events += (A.wp[p + 1] - A.wp[p] + BB - 1) / BB;
+    for (int64_t r = warp - NWC - 1; r < events; r += 2) {
+      const unsigned long long* rec = A.recs + (size_t)(r % kGNB) * NS * G;
       const uint32_t tag = (uint32_t)(r + 1);
-      unsigned long long wv[NQ][2 * NV];
+      unsigned long long wv[NS][NQ];
       bool done;
       do {
+#pragma unroll
+        for (int k = 0; k < NS; ++k)
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+            const int c = lane + 32 * q;
+            wv[k][q] = c < G ? ld_tagged(rec + (size_t)k * G + c) : ((unsigned long long)tag << 32);
+          }
         bool ok = true;
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-          const int c = lane + 32 * q;
-          if (c < G) {
+        for (int k = 0; k < NS; ++k)
 #pragma unroll
-            for (int v = 0; v < NV; ++v)
-              ld_tagged2(rec + (size_t)c * kGRec + 2 * v, wv[q][2 * v], wv[q][2 * v + 1]);
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-          const int c = lane + 32 * q;
-          if (c < G) {
-#pragma unroll
-            for (int k = 0; k < NS; ++k) ok &= (uint32_t)(wv[q][k] >> 32) == tag;
-          }
-        }
+          for (int q = 0; q < NQ; ++q) ok &= (uint32_t)(wv[k][q] >> 32) == tag;
         done = __all_sync(0xffffffffu, ok);
-        if (!done) __nanosleep(64);
+        if (!done) __nanosleep(32);
       } while (!done);
-      float acc[NS];
+      float* t = tot + (r % kGTot) * kGVal;
 #pragma unroll
       for (int k = 0; k < NS; ++k) {
-        acc[k] = 0.f;
+        float acc = 0.f;
 #pragma unroll
-        for (int q = 0; q < NQ; ++q)
-          if (lane + 32 * q < G) acc[k] += __uint_as_float((uint32_t)wv[q][k]);
-        acc[k] = warp_sum(acc[k]);
+        for (int q = 0; q < NQ; ++q) acc += __uint_as_float((uint32_t)wv[k][q]);
+        acc = warp_sum(acc);
+        if (lane == 0) t[k] = acc;
       }
       if (lane == 0) {
         if (A.dbg && cta == 0 && r < 1024) A.dbg[r * 8 + 5] = gtimer_g();
-        float* t = tot + (r % kGTot) * kGRec;
-#pragma unroll
-        for (int k = 0; k < NS; ++k) t[k] = acc[k];
+        if (A.dbg && r < 1024) A.dbg[8192 + 1024 * 160 + r * 160 + cta] = gtimer_g();
         mbar_arrive(&totbar[r % kGTot]);
       }
       __syncwarp();
@@ -249,112 +252,157 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
     const float* ub = A.u + row0 + tid;
     float* outp = A.out + row0 + tid;
     float w[RR];
-    float xr[NS][RR];
+    float xr[NSLOT][BB][RR];
 #pragma unroll
     for (int r = 0; r < RR; ++r) w[r] = r < rmax ? ub[r * NTC] : 0.f;
 #pragma unroll
-    for (int k = 0; k < NS; ++k)
+    for (int sl = 0; sl < NSLOT; ++sl)
 #pragma unroll
-      for (int r = 0; r < RR; ++r) xr[k][r] = 0.f;
+      for (int b = 0; b < BB; ++b)
+#pragma unroll
+        for (int r = 0; r < RR; ++r) xr[sl][b][r] = 0.f;
     const float a = A.a;
     const float inv_a = (float)(1.0 / A.a_d);
     uint32_t stage = 0, phase = 0;
     bool flushed = false;
+    int64_t ebase = 0;  // event (publication) index of the partition's block 0
     for (int p = 0; p < A.n_parts; ++p) {
-      const int64_t pbase = A.wp[p] - s_begin;  // publication index of column 0
+      const int64_t col0 = A.wp[p] - s_begin;  // flattened column index of column 0
       const int m = (int)(A.wp[p + 1] - A.wp[p]);
       if (m == 0) continue;
-      float dh[L];  // deltas of the L most recently resolved columns (dh[0] newest)
+      const int nb = (m + BB - 1) / BB;
+      float dh[LL > 0 ? LL : 1][BB];  // deltas of the LL most recent resolved blocks
 #pragma unroll
-      for (int k = 0; k < L; ++k) dh[k] = 0.f;
-      for (int e0 = 0; e0 < m + L; e0 += NS) {
+      for (int l = 0; l < (LL > 0 ? LL : 1); ++l)
 #pragma unroll
-        for (int i = 0; i < NS; ++i) {
-          const int e = e0 + i;  // e % NS == i: register slot of column e
-          if (e < m + L) {
+        for (int b = 0; b < BB; ++b) dh[l][b] = 0.f;
+      for (int e0 = 0; e0 < nb + LL; e0 += NSLOT) {
+#pragma unroll
+        for (int i = 0; i < NSLOT; ++i) {
+          const int e = e0 + i;  // e % NSLOT == i: register slot of block e
+          if (e < nb + LL) {
             const bool dbg = A.dbg && cta == 0 && tid == 0 && p == 0 && e < 1024;
             if (dbg) A.dbg[e * 8 + 0] = gtimer_g();
-            if (e < m) {
-              // stage column e, publish (s_e, g_e1..g_eL)
-              mbar_wait(&full[stage], phase);
-              if (dbg) A.dbg[e * 8 + 1] = gtimer_g();
-              const float* x = ring + (size_t)stage * CTA_ROWS + tid;
+            if (e < nb) {
+              // ---- stage block e and publish its partials
 #pragma unroll
-              for (int r = 0; r < RR; ++r) xr[i][r] = x[r * NTC];
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&empty[stage]);
-              if (++stage == (uint32_t)S) {
-                stage = 0;
-                phase ^= 1u;
+              for (int b = 0; b < BB; ++b) {
+                if (e * BB + b < m) {
+                  mbar_wait(&full[stage], phase);
+                  const float* x = ring + (size_t)stage * CTA_ROWS + tid;
+#pragma unroll
+                  for (int r = 0; r < RR; ++r) xr[i][b][r] = x[r * NTC];
+                  __syncwarp();
+                  if (lane == 0) mbar_arrive(&empty[stage]);
+                  if (++stage == (uint32_t)S) {
+                    stage = 0;
+                    phase ^= 1u;
+                  }
+                } else {
+#pragma unroll
+                  for (int r = 0; r < RR; ++r) xr[i][b][r] = 0.f;
+                }
               }
+              if (dbg) A.dbg[e * 8 + 1] = gtimer_g();
               float pr[NS];
 #pragma unroll
               for (int k = 0; k < NS; ++k) pr[k] = 0.f;
 #pragma unroll
               for (int r = 0; r < RR; ++r) {
-                const float xv = xr[i][r];
-                pr[0] = fmaf(xv, w[r], pr[0]);
 #pragma unroll
-                for (int k = 1; k <= L; ++k) pr[k] = fmaf(xv, xr[(i + NS - k) % NS][r], pr[k]);
+                for (int b = 0; b < BB; ++b) {
+                  const float xv = xr[i][b][r];
+                  pr[Lay::kS + b] = fmaf(xv, w[r], pr[Lay::kS + b]);
+#pragma unroll
+                  for (int k = 0; k < b; ++k)
+                    pr[Lay::gin(b, k)] = fmaf(xv, xr[i][k][r], pr[Lay::gin(b, k)]);
+#pragma unroll
+                  for (int l = 1; l <= LL; ++l)
+#pragma unroll
+                    for (int k = 0; k < BB; ++k)
+                      pr[Lay::gx(l, b, k)] =
+                          fmaf(xv, xr[(i + NSLOT - l) % NSLOT][k][r], pr[Lay::gx(l, b, k)]);
+                }
               }
 #pragma unroll
               for (int k = 0; k < NS; ++k) pr[k] = warp_sum(pr[k]);
-              const int64_t pub = pbase + e;
+              const int64_t pub = ebase + e;
               const int rb = (int)(pub & 1);
               if (lane == 0) {
 #pragma unroll
-                for (int k = 0; k < NS; ++k) red[(rb * 32 + warp) * kGRec + k] = pr[k];
+                for (int k = 0; k < NS; ++k) red[(rb * 16 + warp) * kGVal + k] = pr[k];
               }
               named_bar_sync(1, NTC);
+              if (A.dbg && warp == 0 && lane == 0 && pub < 1024)
+                A.dbg[8192 + pub * 160 + cta] = gtimer_g();
               if (warp == 0 && lane < NS) {
                 float v = 0.f;
-                for (int q = 0; q < NWC; ++q) v += red[(rb * 32 + q) * kGRec + lane];
-                st_tagged(A.recs + ((size_t)(pub % kGNB) * G + cta) * kGRec + lane,
+                for (int q = 0; q < NWC; ++q) v += red[(rb * 16 + q) * kGVal + lane];
+                st_tagged(A.recs + ((size_t)(pub % kGNB) * NS + lane) * G + cta,
                           (uint32_t)(pub + 1), v);
               }
             }
             if (dbg) A.dbg[e * 8 + 2] = gtimer_g();
-            if (e >= L) {
-              // resolve column c = e - L (register slot (i+1) % NS)
-              const int c = e - L;
-              const int64_t cpub = pbase + c;
+            if (e >= LL) {
+              // ---- resolve block c = e - LL (register slot (i + 1) % NSLOT)
+              const int c = e - LL;
+              const int64_t cpub = ebase + c;
               mbar_wait(&totbar[cpub % kGTot], (uint32_t)((cpub / kGTot) & 1));
               if (dbg) A.dbg[e * 8 + 3] = gtimer_g();
-              const float* t = tot + (cpub % kGTot) * kGRec;
-              float lin = t[0];
+              const float* t = tot + (cpub % kGTot) * kGVal;
+              float dcur[BB];
 #pragma unroll
-              for (int k = 1; k <= L; ++k) lin = fmaf(a * dh[k - 1], t[k], lin);
-              const int4 mt = meta[(A.wp[p] - s_begin + c) & (kGMeta - 1)];
-              const int j = mt.x;
-              const float aj = __int_as_float(mt.y);
-              const float qj = __int_as_float(mt.z);
-              float an;
-              if (A.kind == SYSCD_LOGISTIC_DUAL) {
-                an = (float)coord_step(A.kind, (double)lin, A.a_d, (double)qj, A.lam, (double)aj,
-                                       A.n_coords);
-              } else {
-                an = coord_step_f(A.kind, lin, a, qj, A.lam_f, aj, A.inv_n_f);
+              for (int b = 0; b < BB; ++b) {
+                dcur[b] = 0.f;
+                const int col = c * BB + b;
+                if (col < m) {
+                  float lin = t[Lay::kS + b];
+#pragma unroll
+                  for (int l = 1; l <= LL; ++l)
+#pragma unroll
+                    for (int k = 0; k < BB; ++k)
+                      lin = fmaf(a * dh[l - 1][k], t[Lay::gx(l, b, k)], lin);
+#pragma unroll
+                  for (int k = 0; k < b; ++k) lin = fmaf(a * dcur[k], t[Lay::gin(b, k)], lin);
+                  const int4 mt = meta[(col0 + col) & (kGMeta - 1)];
+                  const int j = mt.x;
+                  const float aj = __int_as_float(mt.y);
+                  const float qj = __int_as_float(mt.z);
+                  float an;
+                  if (A.kind == SYSCD_LOGISTIC_DUAL) {
+                    an = (float)coord_step(A.kind, (double)lin, A.a_d, (double)qj, A.lam,
+                                           (double)aj, A.n_coords);
+                  } else {
+                    an = coord_step_f(A.kind, lin, a, qj, A.lam_f, aj, A.inv_n_f);
+                  }
+                  if (isfinite(an)) {
+                    dcur[b] = an - aj;
+                    if (cta == 0 && tid == 0) A.alpha[j] = an;
+                  } else if (cta == 0 && tid == 0) {
+                    atomicOr(A.status, SYSCD_ENONFINITE);
+                  }
+                }
               }
-              float delta = 0.f;
-              if (isfinite(an)) {
-                delta = an - aj;
-                if (cta == 0 && tid == 0) A.alpha[j] = an;
-              } else if (cta == 0 && tid == 0) {
-                atomicOr(A.status, SYSCD_ENONFINITE);
+#pragma unroll
+              for (int l = LL - 1; l > 0; --l)
+#pragma unroll
+                for (int b = 0; b < BB; ++b) dh[l][b] = dh[l - 1][b];
+              if (LL > 0) {
+#pragma unroll
+                for (int b = 0; b < BB; ++b) dh[0][b] = dcur[b];
               }
 #pragma unroll
-              for (int k = L - 1; k > 0; --k) dh[k] = dh[k - 1];
-              dh[0] = delta;
-              const float sd = a * delta;
-              constexpr int OLD = (0 + 1) % NS;  // placeholder to keep NS in scope
-              (void)OLD;
+              for (int b = 0; b < BB; ++b) {
+                const float sd = a * dcur[b];
 #pragma unroll
-              for (int r = 0; r < RR; ++r) w[r] = fmaf(sd, xr[(i + 1) % NS][r], w[r]);
+                for (int r = 0; r < RR; ++r) w[r] = fmaf(sd, xr[(i + 1) % NSLOT][b][r], w[r]);
+              }
             }
             if (dbg) A.dbg[e * 8 + 4] = gtimer_g();
           }
         }
       }
+      ebase += nb;
       // partition done: fold (w - u)/a into out (one writer per row), reset w
 #pragma unroll
       for (int r = 0; r < RR; ++r) {
@@ -383,33 +431,45 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
 // host side
 // ---------------------------------------------------------------------------
 struct GridEntry {
-  int rr, l;
+  int rr, bb, ll, ns;
   const void* fn;
 };
 
-template <int RR, int L>
+template <int RR, int BB, int LL>
 static GridEntry make_grid() {
-  return {RR, L, (const void*)&k_grid_epoch<RR, L>};
+  return {RR, BB, LL, GridLayout<BB, LL>::kNS, (const void*)&k_grid_epoch<RR, BB, LL>};
 }
 
+// (rows per thread, columns per event, lookahead events).  The default for a
+// given RR is the first entry with that RR; SYSCD_GRID_CFG=<index> overrides.
 static GridEntry g_grid_table[] = {
-    make_grid<4, 6>(), make_grid<8, 5>(), make_grid<12, 4>(), make_grid<17, 3>(),
+    make_grid<4, 2, 2>(),  make_grid<8, 2, 2>(),  make_grid<12, 2, 1>(), make_grid<17, 1, 3>(),
+    make_grid<17, 2, 1>(), make_grid<17, 4, 0>(), make_grid<12, 1, 4>(), make_grid<8, 1, 5>(),
 };
 constexpr int kGridTable = sizeof(g_grid_table) / sizeof(g_grid_table[0]);
+
+static void* g_grid_dbg = nullptr;
 
 int grid_choose(int64_t d, int* idx, int* G, int* stages, size_t* smem_out) {
   int dev = 0, sms = 0, optin = 0;
   SYSCD_CUDA_TRY(cudaGetDevice(&dev));
   SYSCD_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   SYSCD_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const char* force = getenv("SYSCD_GRID_CFG");
   for (int i = 0; i < kGridTable; ++i) {
+    if (force && atoi(force) != i) continue;
+    if (!force) {  // first entry for each RR only
+      bool first = true;
+      for (int k = 0; k < i; ++k) first &= g_grid_table[k].rr != g_grid_table[i].rr;
+      if (!first) continue;
+    }
     const int rows = 416 * g_grid_table[i].rr;
     const int64_t g = (d + rows - 1) / rows;
     if (g > sms) continue;
     const size_t fixed = grid_smem(0, rows).total + 1024;
     int s = (int)(((size_t)optin - 1024 - fixed) / ((size_t)rows * 4));
     s = std::min(s, 8);
-    if (s < 3) continue;
+    if (s < g_grid_table[i].bb + 2) continue;
     *idx = i;
     *G = (int)g;
     *stages = s;
@@ -420,11 +480,7 @@ int grid_choose(int64_t d, int* idx, int* G, int* stages, size_t* smem_out) {
   return SYSCD_EINVAL;
 }
 
-int64_t grid_workspace_bytes(int G) {
-  return (int64_t)kGNB * G * kGRec * 8;
-}
-
-static void* g_grid_dbg = nullptr;
+int64_t grid_workspace_bytes(int G) { return (int64_t)kGNB * kGVal * G * 8; }
 
 int grid_launch(const syscd_dense_epoch_args* e, void* workspace, int64_t ws_bytes,
                 cudaStream_t stream) {

@@ -12,13 +12,16 @@ torch.cuda.set_device(0)
 wl = workload(cfg_id, scale=scale)
 eng = _Engine(wl.problem, wl.solver, Dist())
 eng.global_round(0)
-buf = torch.zeros(1024 * 8, dtype=torch.int64, device="cuda")
+buf = torch.zeros(8192 + 2 * 1024 * 160, dtype=torch.int64, device="cuda")
 L = lib(); L.syscd_debug_set_grid_timeline.argtypes = [ctypes.c_void_p]
 L.syscd_debug_set_grid_timeline(buf.data_ptr())
 eng.global_round(1)
 torch.cuda.synchronize()
 L.syscd_debug_set_grid_timeline(None)
-t = buf.view(1024, 8).cpu().numpy().astype(np.float64)
+allb = buf.cpu().numpy().astype(np.float64)
+t = allb[:8192].reshape(1024, 8)
+pubt = allb[8192:8192 + 1024 * 160].reshape(1024, 160)
+tott = allb[8192 + 1024 * 160:].reshape(1024, 160)
 t = t[100:900]
 ev = np.diff(t[:, 0])
 print(f"mean event {ev.mean():.0f} ns, median {np.median(ev):.0f}")
@@ -33,3 +36,11 @@ ready = t[:, 5]
 need = np.roll(t[:, 2], -Lk)
 print(f"  reducer interval {np.mean(np.diff(ready)):7.0f} ns; slack (need - ready) median {np.median((need-ready)[:-Lk]):7.0f}")
 print(f"  publish(r) -> totals(r) latency median {np.median(ready - t[:,2]):7.0f}")
+
+G = int((pubt[200] > 0).sum())
+P = pubt[100:900, :G]; T = tott[100:900, :G]
+first, last = P.min(axis=1), P.max(axis=1)
+print(f"CTAs {G}: publish skew (last - first) median {np.median(last - first):.0f} ns, p90 {np.percentile(last-first, 90):.0f}")
+print(f"  last publish -> totals (median over CTAs) {np.median(np.median(T, axis=1) - last):.0f} ns")
+print(f"  totals spread across CTAs median {np.median(T.max(axis=1) - T.min(axis=1)):.0f} ns")
+print(f"  CTA0 publish -> last publish {np.median(last - P[:, 0]):.0f} ns")
