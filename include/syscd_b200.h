@@ -169,6 +169,29 @@ typedef struct {
 int syscd_sparse_epoch_workers(int64_t d, int32_t n_parts, int32_t* n_workers);
 int syscd_sparse_epoch(const syscd_sparse_epoch_args* e, void* stream);
 
+/* K = P = 1 primal logistic: exact coordinate updates on the live shared
+ * vector with the reference's safeguarded Newton (solvers.py:403-410,
+ * objective.py:113-184); v (fp64) is updated in place.  Dense (A != NULL) or
+ * CSC store.  One round = the single partition of a K=P=1 plan. */
+typedef struct {
+  int64_t d;
+  int64_t lda;
+  const float* A;
+  const int64_t* col_ptr;
+  const int32_t* row_idx;
+  const float* vals;
+  const float* sq;
+  float* alpha;
+  double* v;
+  const double* y;
+  double lam;
+  const int32_t* seq;
+  const int64_t* work_prefix;
+  int32_t* status;
+} syscd_exact_args;
+
+int syscd_exact_logistic_round(const syscd_exact_args* e, void* stream);
+
 /* ------------------------------------------------------------------------
  * Reduction + epilogue (reduce_replicas solvers.py:112-125 at node/global
  * level, solvers.py:393,423; then grad_f objective.py:105-110 for the next

@@ -50,6 +50,14 @@ class SparseEpochArgs(ctypes.Structure):
     ]
 
 
+class ExactArgs(ctypes.Structure):
+    _fields_ = [
+        ("d", c_i64), ("lda", c_i64), ("A", c_vp), ("col_ptr", c_vp), ("row_idx", c_vp),
+        ("vals", c_vp), ("sq", c_vp), ("alpha", c_vp), ("v", c_vp), ("y", c_vp), ("lam", c_f64),
+        ("seq", c_vp), ("work_prefix", c_vp), ("status", c_vp),
+    ]
+
+
 # (name, restype, argtypes) for every symbol declared in include/syscd_b200.h
 SIGNATURES = {
     "syscd_abi_version": (c_i32, []),
@@ -66,6 +74,7 @@ SIGNATURES = {
     "syscd_dense_epoch": (c_i32, [ctypes.POINTER(DenseEpochArgs), c_vp]),
     "syscd_sparse_epoch_workers": (c_i32, [c_i64, c_i32, ctypes.POINTER(c_i32)]),
     "syscd_sparse_epoch": (c_i32, [ctypes.POINTER(SparseEpochArgs), c_vp]),
+    "syscd_exact_logistic_round": (c_i32, [ctypes.POINTER(ExactArgs), c_vp]),
     "syscd_reduce_partials": (c_i32, [c_vp, c_i64, c_i32, c_i64, c_vp, c_vp]),
     "syscd_apply_dv": (c_i32, [c_i32, c_i64, c_vp, c_vp, c_vp, c_f64, c_f64, c_vp, c_vp]),
     "syscd_grad": (c_i32, [c_i32, c_i64, c_vp, c_vp, c_f64, c_f64, c_vp, c_f64, c_vp, c_vp]),

@@ -23,7 +23,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._lib import DenseEpochArgs, PlanDesc, SparseEpochArgs, call, lib
+from ._lib import DenseEpochArgs, ExactArgs, PlanDesc, SparseEpochArgs, call, lib
 from .device import DeviceProblem, Dist, _ptr, _stream, _torch
 from .objective import LOGISTIC, NonFiniteUpdateError
 from .partitioning import DEFAULT_CACHE_LINE_BYTES, default_bucket_size
@@ -154,10 +154,10 @@ class _Engine:
             self.dp = DeviceProblem(problem, store_cols=sp.store_cols, dist=dist)
         dp = self.dp
         self.single = cfg.K == 1 and cfg.P == 1
-        if self.single and dp.kind == LOGISTIC:
-            raise NotImplementedError(
-                "K=P=1 primal logistic uses the exact Newton path (solvers.py:403-410), "
-                "which is not on the GPU yet; use K*P > 1 or a quadratic objective")
+        # K=P=1 primal logistic: exact Newton updates on the live v
+        # (solvers.py:403-410); every other objective's exact update is the
+        # surrogate step with a = gamma and runs in the epoch kernels
+        self.exact_logistic = self.single and dp.kind == LOGISTIC
         self.a = dp.gamma * cfg.P * cfg.K
         self.n_parts_local = self.K_local * cfg.P
         # planning
@@ -337,10 +337,41 @@ class _Engine:
             if self.kernel_events is not None:
                 self.kernel_events[1].record()
 
+    def exact_round(self, rid):
+        """K=P=1 primal logistic round: exact updates on the live v."""
+        dp = self.dp
+        seq, wp = self.round_tables(rid)
+        if rid >= self.upd_dev.numel():
+            grown = self.torch.zeros(2 * rid + 2, dtype=self.torch.int64, device="cuda")
+            grown[:self.upd_dev.numel()].copy_(self.upd_dev)
+            self.upd_dev = grown
+        self.upd_dev[rid:rid + 1].copy_(wp[1:2])
+        e = ExactArgs()
+        e.d = dp.d
+        if dp.storage == "dense":
+            e.lda = dp.lda
+            e.A = dp.At.data_ptr()
+        else:
+            cp, ri, va = dp.csc
+            e.col_ptr, e.row_idx, e.vals = cp.data_ptr(), ri.data_ptr(), va.data_ptr()
+        e.sq = dp.sq.data_ptr()
+        e.alpha = self.alpha.data_ptr()
+        e.v = self.v.data_ptr()
+        e.y = dp.y.data_ptr()
+        e.lam = dp.lam
+        e.seq = seq.data_ptr()
+        e.work_prefix = wp.data_ptr()
+        e.status = self.status.data_ptr()
+        call("syscd_exact_logistic_round", ctypes.byref(e), _stream())
+
     def global_round(self, t1):
         """One outer round (solvers.py:401-424)."""
         cfg, dp = self.cfg, self.dp
         torch = self.torch
+        if self.exact_logistic:
+            for t2 in range(cfg.T2):
+                self.exact_round(t1 * cfg.T2 + t2)
+            return
         if cfg.T2 == 1:
             self.epoch(t1, self.u)
             self.dist.allreduce_(self.dv)

@@ -62,6 +62,23 @@ def test_trajectory_parity(cuda, cfg_id, scale, kw):
         assert abs(m.gap - r.gap) <= tol + 1e-4 * abs(ores.rows[0].objective)
 
 
+def test_exact_logistic_single_worker(cuda, golden):
+    """K=P=1 primal logistic: the reference's exact Newton path
+    (solvers.py:403-410, objective.py:128-184) vs the oracle."""
+    from oracle import syscd_oracle as O
+    from paper_1911_07722_b200 import (GlmProblem, SmoothLoss, SolverConfig,
+                                       generate_synthetic_dense, run_syscd)
+    for n_rows, n_cols, lam, seed, B, T2 in [(200, 24, 0.5, 3, 4, 1), (300, 37, 0.1, 5, 8, 2)]:
+        ds = generate_synthetic_dense(n_rows, n_cols, seed)
+        pb = GlmProblem.build(ds, SmoothLoss.logistic(), lam)
+        cfg = dict(K=1, P=1, bucket_size=B, T1=4, T2=T2, seed=seed)
+        res = run_syscd(pb, SolverConfig(**cfg))
+        A = ds.matrix.to_dense()
+        ores = O.run_syscd(O.OracleProblem(O.OracleMatrix(dense=A), ds.labels, "logistic", lam),
+                           O.OracleConfig(**cfg))
+        assert_parity(res, ores)
+
+
 def test_full_size_config0_parity(cuda):
     """BASELINE config 0 at full size (20000 x 500, K=1 P=4 B=16), 20 epochs."""
     res, ores = run_pair(0, 1.0, gap=False, K=1, P=4, bucket_size=16, T1=20)
@@ -75,8 +92,6 @@ def test_reference_golden_runs_on_gpu(cuda, golden):
     for case in golden("reference_runs.json"):
         ds = generate_synthetic_dense(case["n_rows"], case["n_cols"], case["data_seed"])
         loss = SmoothLoss.squared_error() if case["loss"] == "squared_error" else SmoothLoss.logistic()
-        if case["loss"] == "logistic" and case["cfg"].get("K", 1) * case["cfg"].get("P", 1) == 1:
-            continue
         pb = GlmProblem.build(ds, loss, case["lam"])
         res = run_syscd(pb, SolverConfig(**case["cfg"]))
         got = np.array([m.objective for m in res.metrics])
