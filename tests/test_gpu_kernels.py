@@ -92,3 +92,17 @@ def test_metrics_kernels_match_numpy(cuda, cfg_id, scale):
     assert gap == pytest.approx(ob.gap(alpha), rel=1e-7, abs=1e-9 * abs(F))
     sq = pb.stats.column_sq_norms
     np.testing.assert_allclose(sq, ob.sq, rtol=1e-6)
+
+
+def test_reference_optimum_ridge_cg(cuda):
+    """GPU CG optimum vs the dense normal-equation solve (cli.py:87-90)."""
+    from paper_1911_07722_b200 import compute_reference_optimum
+    pb, ob = both(0, 0.05)
+    a_star, f_star = compute_reference_optimum(pb)
+    A = ob.A.dense
+    x = np.linalg.solve(A.T @ A + ob.lam * np.eye(A.shape[1]), A.T @ ob.y)
+    assert np.linalg.norm(a_star - x) / np.linalg.norm(x) < 1e-5
+    assert f_star == pytest.approx(ob.objective(x), rel=1e-9)
+    # the dual certificate vanishes at the optimum
+    gap = pb.device().gap_host(a_star)[0]
+    assert gap <= 1e-5 * abs(f_star)  # fp32 alpha, lam=1e-3 amplifies ||A^T w||^2/(2 lam)
