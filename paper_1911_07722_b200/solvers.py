@@ -214,7 +214,9 @@ class _Engine:
             self.partials = torch.empty(d, dtype=torch.float32, device="cuda")
         self.alpha = torch.zeros(dp.n_store, dtype=torch.float32, device="cuda")
         self.v = torch.zeros(d, dtype=torch.float64, device="cuda")
-        self.u = torch.empty(d, dtype=torch.float32, device="cuda")
+        # u is read by 16-byte bulk copies up to round_up(d, 4): pad it
+        self._u_buf = torch.zeros((d + 3) // 4 * 4, dtype=torch.float32, device="cuda")
+        self.u = self._u_buf[:d]
         self.dv = torch.empty(d, dtype=torch.float32, device="cuda")
         self.status = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.kernel_events = None  # (start, stop) CUDA events around the epoch kernel
@@ -381,7 +383,7 @@ class _Engine:
         # T2 > 1: node-local rounds with the drift term (solvers.py:373-398)
         drift = cfg.K * dp.gamma
         delta_sum = torch.zeros(dp.d, dtype=torch.float64, device="cuda")
-        u_k = torch.empty_like(self.u)
+        u_k = torch.zeros_like(self._u_buf)[:dp.d]
         for k in range(self.K_local):
             v_node = self.v.clone()
             for t2 in range(cfg.T2):
