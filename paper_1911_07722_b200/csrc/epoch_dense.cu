@@ -349,27 +349,36 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
         // red.global.add (same thread, same address: applied in program
         // order, so the sum stays deterministic); u comes through the
         // read-only path so the loads issue back to back.
+        // u loads are pipelined one chunk ahead (a compiler barrier keeps
+        // ptxas from hoisting all R of them, which would spill the replica)
+        float ucur[RC], unxt[RC];
+#pragma unroll
+        for (int k = 0; k < RC; ++k) ucur[k] = k < qmax ? __ldg(ub + k * NTC) : 0.f;
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
-          float uu[RC];
+          if (c + 1 < NCH) {
 #pragma unroll
-          for (int k = 0; k < RC; ++k) {
-            const int q = c * RC + k;
-            uu[k] = q < qmax ? __ldg(ub + q * NTC) : 0.f;
+            for (int k = 0; k < RC; ++k) {
+              const int q = (c + 1) * RC + k;
+              unxt[k] = q < qmax ? __ldg(ub + q * NTC) : 0.f;
+            }
           }
+          asm volatile("" ::: "memory");
 #pragma unroll
           for (int k = 0; k < RC; ++k) {
             const int q = c * RC + k;
             if (q < qmax) {
-              const float dv = (w[q] - uu[k]) * inv_a;
+              const float dv = (w[q] - ucur[k]) * inv_a;
               if (flushed) {
                 red_add_f32(out + q * NTC, dv);
               } else {
                 out[q * NTC] = dv;
               }
-              w[q] = uu[k];
+              w[q] = ucur[k];
             }
           }
+#pragma unroll
+          for (int k = 0; k < RC; ++k) ucur[k] = unxt[k];
         }
         flushed = true;
         ++part;
