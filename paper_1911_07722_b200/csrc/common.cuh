@@ -28,17 +28,92 @@ __device__ __forceinline__ double sigmoid_fast(double s) {
   return (double)(s >= 0.0 ? r : e * r);
 }
 
+// Fast path of the logistic-dual coordinate solve (see logistic_dual_solve).
+// Mirror the root into the left half: with C = aq alpha - lin the root of h
+// solves aq sigma(s) = C - s/n; if C > aq/2 substitute s' = -s, which turns it
+// into aq sigma(s') = (aq - C) - s'/n.  So always solve aq sigma(s) = Cl - s/n
+// with Cl <= aq/2 (the root then sits at sigma <= 1/2, where the log form is
+// well conditioned):
+//   * tail (n aq sigma(n Cl) small): the sigmoid term is a small perturbation
+//     of the linear one and the contraction s <- n (Cl - aq sigma(s)) starting
+//     at s = n Cl converges in a few steps;
+//   * otherwise Newton on G(s) = log sigma(s) - log(Cl - s/n) + log aq, which
+//     is monotone and close to linear near the root; ~3 steps from
+//     s0 = logit(Cl / aq).  G is evaluated with fp32 SFU exp/log (the step
+//     only has to land within ~1e-5 of the root).
+// One fp64 Newton step on h itself then polishes the root to the accuracy of
+// the fp32 sigmoid.  Returns false (caller falls back to the bracketed loop)
+// when 8 steps do not converge or the residual of h is not small.
+__device__ __forceinline__ bool logistic_dual_fast(double lin, double aq, double alpha, double n,
+                                                   double* s_out) {
+  const double inv_n = 1.0 / n;
+  const double C = aq * alpha - lin;
+  const bool left = 0.5 * aq - C > 0.0;
+  const double Cl = left ? C : aq - C;
+  const double nCl = n * Cl;
+  const bool tail = n * aq * sigmoid_fast(nCl) < 0.25;
+  const double cap = nCl - 1e-6 * fmax(1.0, fabs(nCl));
+  double sp;
+  if (tail) {
+    sp = nCl;
+  } else {
+    const float r = (float)Cl * __frcp_rn((float)aq);
+    sp = r > 0.f ? (double)(__logf(r) - __logf(1.f - fminf(r, 0.5f))) : nCl - 1.0;
+    sp = fmin(sp, nCl - 1e-3 * fmax(1.0, fabs(nCl)));
+  }
+  const float log_aq = __logf((float)aq);
+  const float inv_n_f = (float)inv_n;
+  bool conv = false;
+#pragma unroll 1
+  for (int it = 0; it < 8; ++it) {
+    double ns;
+    if (tail) {
+      ns = n * (Cl - aq * sigmoid_fast(sp));
+    } else {
+      const double R = Cl - sp * inv_n;
+      if (R > 0.0) {
+        const float sf = (float)sp, Rf = (float)R;
+        const float e = __expf(-fabsf(sf));
+        const float w = __frcp_rn(1.f + e);
+        const float G = fminf(sf, 0.f) - __logf(1.f + e) - __logf(Rf) + log_aq;
+        const float dG = (sf >= 0.f ? e * w : w) + __fdividef(inv_n_f, Rf);
+        ns = fmin(sp - (double)__fdividef(G, dG), cap);
+      } else {
+        ns = 0.5 * (sp + nCl);
+      }
+    }
+    const double step = ns - sp;
+    sp = ns;
+    if (fabs(step) <= 1e-5 * fmax(1.0, fabs(sp))) {
+      conv = true;
+      break;
+    }
+  }
+  const double s = left ? sp : -sp;
+  if (!conv || !isfinite(s)) return false;
+  const double t = sigmoid_fast(s);
+  const double h = lin + aq * (t - alpha) + s * inv_n;
+  const double dh = aq * t * (1.0 - t) + inv_n;
+  if (!(fabs(h) <= 1e-4 * dh * fmax(1.0, fabs(s)))) return false;
+  *s_out = s - h * (double)__frcp_rn((float)dh);
+  return true;
+}
+
 // Root of h(s) = lin + aq (sigma(s) - alpha) + s/n in log-odds s (the oracle's
-// logistic_dual_newton, oracle/objectives.py): bracketed Newton + bisection in
-// fp64, with the sigmoid / logit evaluated by fp32 SFU intrinsics.  The result
-// is stored as fp32 alpha = sigma(s) and sigma' <= 1/4, so the iteration stops
-// at |ds| <= 1e-9 max(1,|s|) (the oracle uses 1e-13 with fp64 transcendentals).
+// logistic_dual_newton, oracle/objectives.py).  logistic_dual_fast handles
+// the common case in ~3 steps; anything it does not certify goes through a
+// bracketed Newton + bisection in fp64 from logit(alpha), with the sigmoid /
+// logit evaluated by fp32 SFU intrinsics.  The result is stored as fp32
+// alpha = sigma(s) and sigma' <= 1/4, so the iteration stops at
+// |ds| <= 1e-9 max(1,|s|) (the oracle uses 1e-13 with fp64 transcendentals).
 __device__ __forceinline__ double logistic_dual_solve(double lin, double aq, double alpha,
                                                       double n) {
+  double s = 0.0;
+  if (aq > 0.0 && logistic_dual_fast(lin, aq, alpha, n, &s)) return sigmoid_fast(s);
   const double inv_n = 1.0 / n;
   double lo = -n * (lin + aq * (1.0 - alpha)) - 1.0;
   double hi = n * (aq * alpha - lin) + 1.0;
-  double s = 0.0;
+  s = 0.0;
   if (alpha > 0.0 && alpha < 1.0) {
     const float af = (float)alpha;
     s = (double)(__logf(af) - __logf(1.f - af));
