@@ -241,6 +241,37 @@ int syscd_gap_terms(int32_t kind, int64_t d, int64_t n, const double* v, const d
                     const double* atw, double lam, double n_coords, double scale, double* out,
                     double* work, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * LIBSVM text ingest (host code; replaces the line loop of load_libsvm,
+ * pkg/src/syscd/dataset.py:169-233).  Two calls over the same byte buffer:
+ * scan validates every line and counts examples / nonzeros, fill writes the
+ * example-major arrays (example e owns entries ex_ptr[e] .. ex_ptr[e+1],
+ * 0-based feature indices ascending).  Lines follow Python's universal
+ * newlines (\n, \r, \r\n); blank lines are skipped but counted; labels and
+ * values follow Python float() and indices Python int() (base 10,
+ * underscores between digits).  The first bad line (lowest line number) is
+ * reported through info->err, exactly as the reference's ValueErrors:
+ *   1 bad label, 2 bad entry, 3 index not 1-based, 4 indices not ascending,
+ *   5 index beyond int32 (this store's limit).                            */
+typedef struct {
+  int64_t n_examples;  /* non-blank lines */
+  int64_t nnz;
+  int64_t max_feature; /* largest 1-based index (0 if none) */
+  int32_t err;         /* 0 = ok, else the code above */
+  int32_t pad_;
+  int64_t err_line;    /* 1-based line of the first error */
+  int64_t err_tok_off; /* offending token: byte offset and length in buf */
+  int64_t err_tok_len;
+  int64_t err_index;   /* the parsed index for codes 3 and 5 */
+} syscd_libsvm_info;
+
+int syscd_libsvm_scan(const char* buf, int64_t len, int32_t n_threads, syscd_libsvm_info* info);
+int syscd_libsvm_fill(const char* buf, int64_t len, int32_t n_threads, double* labels,
+                      int64_t* ex_ptr, int32_t* feat_idx, double* vals);
+/* CSR -> CSC transpose on the host (stable: rows stay ascending per column). */
+int syscd_csr_transpose(int64_t n_rows, int64_t n_cols, const int64_t* ptr, const int32_t* idx,
+                        const double* vals, int64_t* t_ptr, int32_t* t_idx, double* t_vals);
+
 #ifdef __cplusplus
 }
 #endif

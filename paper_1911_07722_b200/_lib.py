@@ -50,6 +50,14 @@ class SparseEpochArgs(ctypes.Structure):
     ]
 
 
+class LibsvmInfo(ctypes.Structure):
+    _fields_ = [
+        ("n_examples", c_i64), ("nnz", c_i64), ("max_feature", c_i64), ("err", c_i32),
+        ("pad_", c_i32), ("err_line", c_i64), ("err_tok_off", c_i64), ("err_tok_len", c_i64),
+        ("err_index", c_i64),
+    ]
+
+
 class ExactArgs(ctypes.Structure):
     _fields_ = [
         ("d", c_i64), ("lda", c_i64), ("A", c_vp), ("col_ptr", c_vp), ("row_idx", c_vp),
@@ -89,6 +97,9 @@ SIGNATURES = {
                                       c_vp, c_vp]),
     "syscd_gap_terms": (c_i32, [c_i32, c_i64, c_i64, c_vp, c_vp, c_vp, c_f64, c_f64, c_f64, c_vp,
                                 c_vp, c_vp]),
+    "syscd_libsvm_scan": (c_i32, [c_vp, c_i64, c_i32, ctypes.POINTER(LibsvmInfo)]),
+    "syscd_libsvm_fill": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp]),
+    "syscd_csr_transpose": (c_i32, [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
 }
 
 _lib = None

@@ -237,3 +237,108 @@ def generate_synthetic_sparse(n_examples, n_features, density, seed):
         cols.append((idx, g.random(idx.size)))
     labels = _rng(seed, _SYNTH_LABELS).integers(0, 2, size=n_examples) * 2.0 - 1.0
     return LabeledDataset(ColumnMatrix(n_examples, n_features, sparse_cols=cols), labels)
+
+
+# ---------------------------------------------------------------------------
+# LIBSVM text ingest / export (dataset.py:169-259)
+# ---------------------------------------------------------------------------
+def _nonfinite_column(ptr, vals):
+    bad = np.flatnonzero(~np.isfinite(vals))
+    return int(np.searchsorted(ptr, bad[0], side="right") - 1)
+
+
+def load_libsvm(path, n_features=None, orientation=COORDINATES_ARE_FEATURES, n_threads=0):
+    """Parse a LIBSVM text file (1-based ascending feature indices) into a
+    LabeledDataset in the requested orientation (dataset.py:169-233).
+
+    The text is parsed by the library's multi-threaded host parser
+    (syscd_libsvm_scan / syscd_libsvm_fill); the errors are the reference's
+    ValueErrors with the same line numbers and messages.  The feature
+    orientation transposes the example-major arrays into CSC (rows of a
+    column ascending).  Values are stored float32 like every ColumnMatrix;
+    labels stay float64.
+    """
+    import ctypes
+    from . import _lib
+    if orientation not in (COORDINATES_ARE_FEATURES, COORDINATES_ARE_EXAMPLES):
+        raise ValueError(f"unknown orientation: {orientation}")
+    with open(path, "rb") as fh:
+        buf = fh.read()
+    cbuf = ctypes.cast(ctypes.c_char_p(buf), ctypes.c_void_p)
+    info = _lib.LibsvmInfo()
+    _lib.call("syscd_libsvm_scan", cbuf, len(buf), int(n_threads), ctypes.byref(info))
+    if info.err:
+        line = info.err_line
+        tok = buf[info.err_tok_off:info.err_tok_off + info.err_tok_len].decode(errors="replace")
+        msg = {
+            1: f"bad label {tok!r}",
+            2: f"bad entry {tok!r}",
+            3: f"index {info.err_index} is not 1-based",
+            4: "indices not ascending",
+            5: f"index {info.err_index} exceeds the int32 row-index store",
+        }[info.err]
+        raise ValueError(f"line {line}: {msg}")
+    nex, nnz = int(info.n_examples), int(info.nnz)
+    if nex == 0:
+        raise ValueError("empty dataset")
+    nfeat = max(int(info.max_feature), n_features or 0)
+    if nfeat == 0:
+        raise ValueError("dataset has no features")
+    labels = np.empty(nex, dtype=np.float64)
+    ex_ptr = np.empty(nex + 1, dtype=np.int64)
+    feat = np.empty(max(nnz, 1), dtype=np.int32)
+    vals = np.empty(max(nnz, 1), dtype=np.float64)
+    _lib.call("syscd_libsvm_fill", cbuf, len(buf), int(n_threads), labels.ctypes.data,
+              ex_ptr.ctypes.data, feat.ctypes.data, vals.ctypes.data)
+    feat, vals = feat[:nnz], vals[:nnz]
+    if orientation == COORDINATES_ARE_EXAMPLES:
+        if not np.all(np.isfinite(vals)):
+            raise ValueError(f"column {_nonfinite_column(ex_ptr, vals)}: non-finite values")
+        matrix = ColumnMatrix(nfeat, nex, csc=(ex_ptr, feat, vals))
+        return LabeledDataset(matrix, labels, orientation)
+    col_ptr = np.empty(nfeat + 1, dtype=np.int64)
+    rows = np.empty(max(nnz, 1), dtype=np.int32)
+    cvals = np.empty(max(nnz, 1), dtype=np.float64)
+    _lib.call("syscd_csr_transpose", nex, nfeat, ex_ptr.ctypes.data, feat.ctypes.data,
+              vals.ctypes.data, col_ptr.ctypes.data, rows.ctypes.data, cvals.ctypes.data)
+    rows, cvals = rows[:nnz], cvals[:nnz]
+    if not np.all(np.isfinite(cvals)):
+        raise ValueError(f"column {_nonfinite_column(col_ptr, cvals)}: non-finite values")
+    matrix = ColumnMatrix(nex, nfeat, csc=(col_ptr, rows, cvals))
+    return LabeledDataset(matrix, labels, orientation)
+
+
+def save_libsvm(dataset, path):
+    """Write a feature-oriented LabeledDataset as LIBSVM text with 17
+    significant digits (dataset.py:236-259), so a reload reproduces the
+    stored values exactly."""
+    from . import _lib
+    if dataset.orientation != COORDINATES_ARE_FEATURES:
+        raise ValueError("save_libsvm expects the feature orientation")
+    m = dataset.matrix
+    if m.storage_kind == "dense":
+        dense = m._host_dense()
+        rr, cc = np.nonzero(dense.T)  # column-major walk: (feature, example)
+        order = np.lexsort((rr, cc))
+        feats, exs = rr[order], cc[order]
+        vals = dense[exs, feats].astype(np.float64)
+        ex_ptr = np.zeros(m.n_rows + 1, dtype=np.int64)
+        np.add.at(ex_ptr, exs + 1, 1)
+        ex_ptr = np.cumsum(ex_ptr)
+    else:
+        col_ptr, rows, cvals = m.csc()
+        nnz = int(col_ptr[-1])
+        ex_ptr = np.empty(m.n_rows + 1, dtype=np.int64)
+        feats = np.empty(max(nnz, 1), dtype=np.int32)
+        vals = np.empty(max(nnz, 1), dtype=np.float64)
+        cv64 = np.ascontiguousarray(cvals, dtype=np.float64)
+        _lib.call("syscd_csr_transpose", m.n_cols, m.n_rows, np.ascontiguousarray(col_ptr).ctypes.data,
+                  np.ascontiguousarray(rows).ctypes.data, cv64.ctypes.data, ex_ptr.ctypes.data,
+                  feats.ctypes.data, vals.ctypes.data)
+        feats, vals = feats[:nnz], vals[:nnz]
+    with open(path, "w") as fh:
+        for i in range(m.n_rows):
+            a, b = ex_ptr[i], ex_ptr[i + 1]
+            toks = ["%.17g" % dataset.labels[i]]
+            toks += ["%d:%.17g" % (int(j) + 1, float(v)) for j, v in zip(feats[a:b], vals[a:b])]
+            fh.write(" ".join(toks) + "\n")
