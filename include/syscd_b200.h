@@ -193,6 +193,39 @@ typedef struct {
 int syscd_exact_logistic_round(const syscd_exact_args* e, void* stream);
 
 /* ------------------------------------------------------------------------
+ * Wild (asynchronous) epoch: run_wild_parallel_scd's worker loop
+ * (solvers.py:214-286).  Worker w < P walks chunk w of np.array_split(perm,
+ * P) with exact updates on the live shared vector v = v0 + dv: lin =
+ * x_j . (u + gamma dv) with u = grad f(v0) (exact for the quadratic f of
+ * ridge / lasso / svm-dual / logistic-dual; primal logistic goes through
+ * syscd_exact_logistic_round).  dv (fp32, zero at the epoch start) is read
+ * through L2 and updated with unsynchronised atomics, so results depend on
+ * the hardware interleaving exactly as the reference's threads do.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  int32_t kind;
+  int64_t d;
+  int64_t lda;            /* dense store (A != NULL) */
+  const float* A;
+  const int64_t* col_ptr; /* CSC store (A == NULL) */
+  const int32_t* row_idx;
+  const float* vals;
+  const float* sq;
+  float* alpha;
+  const float* u;
+  float* dv;
+  const int32_t* perm;    /* n store-column ids, this epoch's permutation */
+  int64_t n;
+  int32_t P;
+  double gamma;
+  double lam;
+  double n_coords;
+  int32_t* status;
+} syscd_wild_epoch_args;
+
+int syscd_wild_epoch(const syscd_wild_epoch_args* e, void* stream);
+
+/* ------------------------------------------------------------------------
  * Reduction + epilogue (reduce_replicas solvers.py:112-125 at node/global
  * level, solvers.py:393,423; then grad_f objective.py:105-110 for the next
  * round, solvers.py:412).

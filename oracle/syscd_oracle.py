@@ -470,3 +470,46 @@ def run_syscd(pb: OracleProblem, cfg: OracleConfig, init_alpha=None):
             converged = True
             break
     return OracleResult(alpha, rows, converged, total, diverged, snaps, v)
+
+
+def run_wild(pb: OracleProblem, cfg: OracleConfig):
+    """run_wild_parallel_scd (solvers.py:214-286) with the P chunks of
+    np.array_split(perm, P) run back to back: for P = 1 this is the
+    reference's (deterministic) schedule; for P > 1 it is the zero-staleness
+    interleaving of the asynchronous workers.  Exact updates on the live v
+    (exact_coordinate_update, objective.py:113-125)."""
+    n = pb.n
+    alpha = np.zeros(n)
+    v = np.zeros(pb.d)
+    init = pb.objective(alpha)
+    rows = [OracleRow(0, init, 0.0, 0, np.inf)]
+    prev = alpha.copy()
+    total = 0
+    converged = diverged = False
+    for epoch in range(cfg.n_rounds):
+        perm = stream(cfg.seed, (COORD_PERM, epoch, 0)).permutation(n)
+        failed = False
+        upd = 0
+        for chunk in np.array_split(perm, cfg.P):
+            for j in chunk:
+                j = int(j)
+                delta = pb.exact_delta(j, alpha[j], v)
+                if not np.isfinite(delta):
+                    failed = True
+                    break
+                alpha[j] += delta
+                pb.A.col_axpy(v, j, delta)
+                upd += 1
+        total += upd
+        obj = pb.objective(alpha) if np.all(np.isfinite(alpha)) else np.inf
+        if failed or not np.isfinite(obj) or obj > 1e6 * max(init, 1e-300):
+            rows.append(OracleRow(epoch + 1, obj, 0.0, upd, np.inf))
+            diverged = True
+            break
+        rel = _rel_change(alpha, prev)
+        prev = alpha.copy()
+        rows.append(OracleRow(epoch + 1, obj, 0.0, upd, rel))
+        if cfg.T1 is None and rel < cfg.tolerance:
+            converged = True
+            break
+    return OracleResult(alpha, rows, converged, total, diverged, [], v)

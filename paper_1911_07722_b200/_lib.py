@@ -58,6 +58,15 @@ class LibsvmInfo(ctypes.Structure):
     ]
 
 
+class WildEpochArgs(ctypes.Structure):
+    _fields_ = [
+        ("kind", c_i32), ("d", c_i64), ("lda", c_i64), ("A", c_vp), ("col_ptr", c_vp),
+        ("row_idx", c_vp), ("vals", c_vp), ("sq", c_vp), ("alpha", c_vp), ("u", c_vp),
+        ("dv", c_vp), ("perm", c_vp), ("n", c_i64), ("P", c_i32), ("gamma", c_f64),
+        ("lam", c_f64), ("n_coords", c_f64), ("status", c_vp),
+    ]
+
+
 class ExactArgs(ctypes.Structure):
     _fields_ = [
         ("d", c_i64), ("lda", c_i64), ("A", c_vp), ("col_ptr", c_vp), ("row_idx", c_vp),
@@ -97,6 +106,7 @@ SIGNATURES = {
                                       c_vp, c_vp]),
     "syscd_gap_terms": (c_i32, [c_i32, c_i64, c_i64, c_vp, c_vp, c_vp, c_f64, c_f64, c_f64, c_vp,
                                 c_vp, c_vp]),
+    "syscd_wild_epoch": (c_i32, [ctypes.POINTER(WildEpochArgs), c_vp]),
     "syscd_libsvm_scan": (c_i32, [c_vp, c_i64, c_i32, ctypes.POINTER(LibsvmInfo)]),
     "syscd_libsvm_fill": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "syscd_csr_transpose": (c_i32, [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),

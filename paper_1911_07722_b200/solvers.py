@@ -23,7 +23,8 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._lib import DenseEpochArgs, ExactArgs, PlanDesc, SparseEpochArgs, call, lib
+from ._lib import (DenseEpochArgs, ExactArgs, PlanDesc, SparseEpochArgs, WildEpochArgs, call,
+                   lib)
 from .device import DeviceProblem, Dist, _ptr, _stream, _torch
 from .objective import LOGISTIC, NonFiniteUpdateError
 from .partitioning import DEFAULT_CACHE_LINE_BYTES, default_bucket_size
@@ -452,20 +453,119 @@ def run_syscd(problem, cfg, f_star=None, dist=None):
 
 
 def run_sequential_scd(problem, cfg, f_star=None, dist=None):
-    """Sequential SCD (solvers.py:181-211): the K=P=1 round with exact
-    updates, which is what run_syscd does for K=P=1 (solvers.py:403-410)."""
+    """Sequential SCD (solvers.py:181-211): one node, one thread, exact
+    updates over the shuffled buckets, i.e. run_syscd's K=P=1 round
+    (solvers.py:403-410).  Like the reference it ignores cfg.K / P / T2."""
     if cfg.algorithm != "sequential":
         raise ValueError("config.algorithm must be 'sequential'")
-    if cfg.K != 1 or cfg.P != 1:
-        raise ValueError("sequential solver runs on one thread")
     import dataclasses
-    return _run(problem, dataclasses.replace(cfg, algorithm="syscd"), f_star, dist)
+    one = dataclasses.replace(cfg, algorithm="syscd", K=1, P=1, T2=1)
+    return _run(problem, one, f_star, dist)
 
 
 def run_wild_parallel_scd(problem, cfg, f_star=None):
-    raise NotImplementedError(
-        "the PASSCoDe-wild baseline (solvers.py:214-286) is outside this framework's scope "
-        "(SURVEY 2, row 4)")
+    """Asynchronous parallel SCD (solvers.py:214-286) on one GPU.
+
+    Every epoch draws the permutation of all n coordinates with key
+    (COORD_PERM, epoch, 0) (:250), splits it like np.array_split into P
+    chunks and runs P workers that update the shared alpha and v without
+    synchronisation (syscd_wild_epoch; primal logistic runs the chunks back
+    to back through the exact Newton kernel).  Metrics, divergence handling
+    (a non-finite step or F > 1e6 F(0) ends the run with a diverged row) and
+    the stopping rule follow :236-282.
+    """
+    from .partitioning import COORD_PERM, RngStream, permute_within_bucket
+    if cfg.algorithm != "wild":
+        raise ValueError("config.algorithm must be 'wild'")
+    if cfg.K != 1:
+        raise ValueError("wild solver uses a flat thread pool (K must be 1)")
+    torch = _torch()
+    if problem._device is None:
+        problem._device = DeviceProblem(problem, dist=Dist())
+    dp = problem._device
+    n, d = dp.n_global, dp.d
+    f32 = torch.float32
+    alpha = torch.zeros(dp.n_store, dtype=f32, device="cuda")
+    v = torch.zeros(d, dtype=torch.float64, device="cuda")
+    u_buf = torch.zeros((d + 3) // 4 * 4, dtype=f32, device="cuda")
+    dv_buf = torch.zeros_like(u_buf)
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    perm_host = torch.empty(max(n, 1), dtype=torch.int32, pin_memory=True)
+    perm_dev = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    wp = torch.tensor([0, n], dtype=torch.int64, device="cuda")
+    dp.grad_into(v, u_buf[:d])
+    logistic = dp.kind == LOGISTIC
+
+    def evaluate():
+        if cfg.compute_gap:
+            gap, obj = dp.gap(alpha)
+            return obj, gap
+        return dp.objective(alpha), None
+
+    init_obj, gap0 = evaluate()
+    metrics = [EpochMetrics(0, init_obj, init_obj - f_star if f_star is not None else None,
+                            0.0, 0, np.inf, gap0)]
+    snaps = []
+    prev = alpha.clone()
+    converged = diverged = False
+    total = 0
+    for epoch in range(cfg.n_rounds):
+        t0 = time.perf_counter()
+        perm = permute_within_bucket((0, n), RngStream(cfg.seed, (COORD_PERM, epoch, 0)))
+        perm_host.numpy()[:n] = perm
+        perm_dev.copy_(perm_host, non_blocking=True)
+        if logistic:
+            e = ExactArgs()
+            e.d = dp.d
+            if dp.storage == "dense":
+                e.lda, e.A = dp.lda, dp.At.data_ptr()
+            else:
+                cp, ri, va = dp.csc
+                e.col_ptr, e.row_idx, e.vals = cp.data_ptr(), ri.data_ptr(), va.data_ptr()
+            e.sq, e.alpha, e.v, e.y = (dp.sq.data_ptr(), alpha.data_ptr(), v.data_ptr(),
+                                        dp.y.data_ptr())
+            e.lam = dp.lam
+            e.seq, e.work_prefix, e.status = perm_dev.data_ptr(), wp.data_ptr(), status.data_ptr()
+            call("syscd_exact_logistic_round", ctypes.byref(e), _stream())
+        else:
+            w = WildEpochArgs()
+            w.kind, w.d = dp.kind, dp.d
+            if dp.storage == "dense":
+                w.lda, w.A = dp.lda, dp.At.data_ptr()
+            else:
+                cp, ri, va = dp.csc
+                w.col_ptr, w.row_idx, w.vals = cp.data_ptr(), ri.data_ptr(), va.data_ptr()
+            w.sq, w.alpha, w.u, w.dv = (dp.sq.data_ptr(), alpha.data_ptr(), u_buf.data_ptr(),
+                                        dv_buf.data_ptr())
+            w.perm, w.n, w.P = perm_dev.data_ptr(), n, int(cfg.P)
+            w.gamma, w.lam, w.n_coords = dp.gamma, dp.lam, dp.n_coords
+            w.status = status.data_ptr()
+            call("syscd_wild_epoch", ctypes.byref(w), _stream())
+            call("syscd_apply_dv", dp.kind, dp.d, _ptr(dv_buf), _ptr(v), _ptr(dp.y), dp.lam,
+                 dp.n_coords, _ptr(u_buf), _stream())
+            dv_buf.zero_()
+        failed = bool(int(status.item()) & 2)  # synchronises
+        elapsed = time.perf_counter() - t0
+        upd = n
+        total += upd
+        finite = bool(torch.isfinite(alpha).all())
+        obj, gap = evaluate() if finite else (np.inf, None)
+        if failed or not np.isfinite(obj) or obj > DIVERGENCE_FACTOR * max(init_obj, 1e-300):
+            metrics.append(EpochMetrics(epoch + 1, obj, None, elapsed, upd, np.inf))
+            diverged = True
+            break
+        rel = _rel_change(alpha, prev)
+        prev.copy_(alpha)
+        sub = obj - f_star if f_star is not None else None
+        metrics.append(EpochMetrics(epoch + 1, obj, sub, elapsed, upd, rel, gap))
+        if cfg.record_alpha:
+            snaps.append(alpha.double().cpu().numpy())
+        if cfg.T1 is None and rel < cfg.tolerance:
+            converged = True
+            break
+    return TrainResult(alpha.double().cpu().numpy(), metrics, converged, total,
+                       diverged=diverged, reason="diverged" if diverged else None,
+                       alpha_snapshots=snaps)
 
 
 def run_solver(problem, cfg, f_star=None):

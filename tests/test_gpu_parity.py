@@ -193,8 +193,8 @@ def test_errors(cuda):
         run_syscd(pb, SolverConfig(K=2, P=2, bucket_size=4))
     with pytest.raises(ValueError):
         run_syscd(pb, SolverConfig(algorithm="sequential"))
-    with pytest.raises(NotImplementedError):
-        run_solver(pb, SolverConfig(algorithm="wild", T1=1))
+    res = run_solver(pb, SolverConfig(algorithm="wild", T1=1))  # dispatches to the wild solver
+    assert len(res.metrics) == 2 and res.total_updates == 8
     big = np.full((64, 4), 3e38, dtype=np.float64)
     ds = LabeledDataset(ColumnMatrix(64, 4, dense=big), np.ones(64))
     bad = GlmProblem.build(ds, SmoothLoss.squared_error(), 1.0)

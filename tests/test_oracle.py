@@ -32,6 +32,24 @@ def test_oracle_reproduces_reference_runs_bitwise(golden):
         assert res.alpha.tolist() == case["alpha"]
 
 
+def test_oracle_reproduces_reference_wild_and_sequential_bitwise(golden):
+    """run_wild_parallel_scd (P = 1) and run_sequential_scd (which ignores K
+    and P) of the reference, tests/golden/wild_runs.json."""
+    import dataclasses
+    for case in golden("wild_runs.json"):
+        A, y = _ref_dense(case["n_rows"], case["n_cols"], case["data_seed"])
+        kind = "ridge" if case["loss"] == "squared_error" else "logistic"
+        pb = O.OracleProblem(O.OracleMatrix(dense=A), y, kind, case["lam"])
+        cfg = O.OracleConfig(**case["cfg"])
+        if case["solver"] == "wild":
+            res = O.run_wild(pb, cfg)
+        else:
+            res = O.run_syscd(pb, dataclasses.replace(cfg, K=1, P=1))
+        assert [r.objective for r in res.rows] == case["objective"], case["cfg"]
+        assert [r.updates for r in res.rows] == case["updates"]
+        assert res.alpha.tolist() == case["alpha"]
+
+
 def test_oracle_matches_reference_driver_on_extended_objectives(golden):
     for case in golden("extended_runs.json"):
         A = np.asfortranarray(np.array(case["A"]))
