@@ -100,3 +100,19 @@ def test_shard_plan_single_and_errors(built_lib):
         shard_plan(16, 8, 2, 2, seed=0)
     with pytest.raises(ValueError):
         shard_plan(100, 8, 3, 1, seed=0, world=2, rank=0)
+
+
+def test_spec_validation_and_thread_split():
+    from paper_1911_07722_b200 import SolverConfig
+    from paper_1911_07722_b200.experiment import ExperimentSpec, split_threads
+    base = SolverConfig()
+    with pytest.raises(ValueError, match="exactly one dataset source"):
+        ExperimentSpec("syscd", None, None, None, "squared", 1.0, 1, [1], [8], base, "a", "b")
+    with pytest.raises(ValueError, match="nonempty"):
+        ExperimentSpec("syscd", None, (10, 2), None, "squared", 1.0, 1, [], [8], base, "a", "b")
+    assert split_threads("syscd", 8, 2) == (2, 4)
+    assert split_threads("wild", 8, 1) == (1, 8)
+    with pytest.raises(ValueError):
+        split_threads("syscd", 6, 4)
+    with pytest.raises(ValueError):
+        split_threads("sequential", 2, 1)
