@@ -28,6 +28,12 @@ __device__ __forceinline__ double sigmoid_fast(double s) {
   return (double)(s >= 0.0 ? r : e * r);
 }
 
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 // Fast path of the logistic-dual coordinate solve (see logistic_dual_solve).
 // Mirror the root into the left half: with C = aq alpha - lin the root of h
 // solves aq sigma(s) = C - s/n; if C > aq/2 substitute s' = -s, which turns it
@@ -39,8 +45,9 @@ __device__ __forceinline__ double sigmoid_fast(double s) {
 //     at s = n Cl converges in a few steps;
 //   * otherwise Newton on G(s) = log sigma(s) - log(Cl - s/n) + log aq, which
 //     is monotone and close to linear near the root; ~3 steps from
-//     s0 = logit(Cl / aq).  G is evaluated with fp32 SFU exp/log (the step
-//     only has to land within ~1e-5 of the root).
+//     s0 = logit(Cl / aq).
+// Both iterations run in fp32 with SFU exp / log / rcp (they only have to
+// land within ~1e-5 of the root).
 // One fp64 Newton step on h itself then polishes the root to the accuracy of
 // the fp32 sigmoid.  Returns false (caller falls back to the bracketed loop)
 // when 8 steps do not converge or the residual of h is not small.
@@ -50,52 +57,54 @@ __device__ __forceinline__ bool logistic_dual_fast(double lin, double aq, double
   const double C = aq * alpha - lin;
   const bool left = 0.5 * aq - C > 0.0;
   const double Cl = left ? C : aq - C;
-  const double nCl = n * Cl;
-  const bool tail = n * aq * sigmoid_fast(nCl) < 0.25;
-  const double cap = nCl - 1e-6 * fmax(1.0, fabs(nCl));
-  double sp;
+  // the iteration runs in fp32 (the fp64 polish below restores accuracy)
+  const float aqf = (float)aq, nf = (float)n, inv_nf = (float)inv_n;
+  const float Clf = (float)Cl, nClf = (float)(n * Cl);
+  const float e0 = __expf(-fabsf(nClf));
+  const float sig0 = nClf >= 0.f ? rcp_approx(1.f + e0) : e0 * rcp_approx(1.f + e0);
+  const bool tail = nf * aqf * sig0 < 0.25f;
+  const float cap = nClf - 1e-6f * fmaxf(1.f, fabsf(nClf));
+  float sp;
   if (tail) {
-    sp = nCl;
+    sp = nClf;
   } else {
-    const float r = (float)Cl * __frcp_rn((float)aq);
-    sp = r > 0.f ? (double)(__logf(r) - __logf(1.f - fminf(r, 0.5f))) : nCl - 1.0;
-    sp = fmin(sp, nCl - 1e-3 * fmax(1.0, fabs(nCl)));
+    const float r = Clf * rcp_approx(aqf);
+    sp = r > 0.f ? __logf(r) - __logf(1.f - fminf(r, 0.5f)) : nClf - 1.f;
+    sp = fminf(sp, nClf - 1e-3f * fmaxf(1.f, fabsf(nClf)));
   }
-  const float log_aq = __logf((float)aq);
-  const float inv_n_f = (float)inv_n;
+  const float log_aq = __logf(aqf);
   bool conv = false;
 #pragma unroll 1
   for (int it = 0; it < 8; ++it) {
-    double ns;
+    const float e = __expf(-fabsf(sp));
+    const float w = rcp_approx(1.f + e);
+    float ns;
     if (tail) {
-      ns = n * (Cl - aq * sigmoid_fast(sp));
+      ns = nf * (Clf - aqf * (sp >= 0.f ? w : e * w));
     } else {
-      const double R = Cl - sp * inv_n;
-      if (R > 0.0) {
-        const float sf = (float)sp, Rf = (float)R;
-        const float e = __expf(-fabsf(sf));
-        const float w = __frcp_rn(1.f + e);
-        const float G = fminf(sf, 0.f) - __logf(1.f + e) - __logf(Rf) + log_aq;
-        const float dG = (sf >= 0.f ? e * w : w) + __fdividef(inv_n_f, Rf);
-        ns = fmin(sp - (double)__fdividef(G, dG), cap);
+      const float R = Clf - sp * inv_nf;
+      if (R > 0.f) {
+        const float G = fminf(sp, 0.f) - __logf(1.f + e) - __logf(R) + log_aq;
+        const float dG = (sp >= 0.f ? e * w : w) + inv_nf * rcp_approx(R);
+        ns = fminf(sp - G * rcp_approx(dG), cap);
       } else {
-        ns = 0.5 * (sp + nCl);
+        ns = 0.5f * (sp + nClf);
       }
     }
-    const double step = ns - sp;
+    const float step = ns - sp;
     sp = ns;
-    if (fabs(step) <= 1e-5 * fmax(1.0, fabs(sp))) {
+    if (fabsf(step) <= 1e-5f * fmaxf(1.f, fabsf(sp))) {
       conv = true;
       break;
     }
   }
-  const double s = left ? sp : -sp;
+  const double s = left ? (double)sp : -(double)sp;
   if (!conv || !isfinite(s)) return false;
   const double t = sigmoid_fast(s);
   const double h = lin + aq * (t - alpha) + s * inv_n;
   const double dh = aq * t * (1.0 - t) + inv_n;
   if (!(fabs(h) <= 1e-4 * dh * fmax(1.0, fabs(s)))) return false;
-  *s_out = s - h * (double)__frcp_rn((float)dh);
+  *s_out = s - h * (double)rcp_approx((float)dh);
   return true;
 }
 

@@ -108,6 +108,8 @@ __global__ void __launch_bounds__(32 * kSparseWarps) k_sparse_epoch(SparseArgs A
   const int64_t p_hi = g == W - 1 ? A.n_parts : lb_i64(A.wp, A.n_parts + 1, t_hi);
   float* dv = A.dv_work + (int64_t)g * A.d;
   const float a = A.a;
+  for (int k = lane; k < kTable; k += 32) S.key[k] = kEmpty;
+  __syncwarp();
 
   for (int64_t p = p_lo; p < p_hi; ++p) {
     const int64_t s0 = A.wp[p], s1 = A.wp[p + 1];
@@ -162,8 +164,8 @@ __global__ void __launch_bounds__(32 * kSparseWarps) k_sparse_epoch(SparseArgs A
         c0 += 1;
         continue;
       }
-      // ---- stage the chunk's nonzeros and hash their rows
-      for (int k = lane; k < kTable; k += 32) S.key[k] = kEmpty;
+      // ---- stage the chunk's nonzeros and hash their rows (the table is
+      // empty here: cleared once at start, used slots reset at writeback)
       if (lane < m) {
         S.col_j[lane] = j;
         S.col_pre[lane + 1] = pre;
@@ -296,16 +298,18 @@ __global__ void __launch_bounds__(32 * kSparseWarps) k_sparse_epoch(SparseArgs A
         if (lane == 0 && isfinite(an)) A.alpha[jt] = aj + delta;
         __syncwarp();
       }
-      // ---- write back every distinct row once
-      for (int h = lane; h < kTable; h += 32) {
-        const int r = S.key[h];
-        if (r != kEmpty) {
-          const float c = S.acc[h];
-          if (c != 0.f) {
-            dv[r] = S.dvold[h] + c;
-            red_add_f32(A.delta_v + r, c);
-          }
+      // ---- write back every distinct row once (by the lane that inserted
+      // it) and release its slot
+      for (unsigned o = own; o; o &= o - 1) {
+        const int e = lane + 32 * (__ffs(o) - 1);
+        const int h = S.slot[e];
+        const int r = S.row[e];
+        const float c = S.acc[h];
+        if (c != 0.f) {
+          dv[r] = S.dvold[h] + c;
+          red_add_f32(A.delta_v + r, c);
         }
+        S.key[h] = kEmpty;
       }
       __syncwarp();
       c0 += m;
