@@ -142,10 +142,14 @@ int syscd_dense_epoch(const syscd_dense_epoch_args* e, void* stream);
 
 
 /* Sparse CSC store (int64 col_ptr, int32 row_idx, fp32 values); sparse
- * col_dot / col_axpy of dataset.py:77-78,90-91.  One warp per worker; each
- * worker's private replica row of dv_work (n_workers x d fp32) must be all-zero
- * on entry and is all-zero again on return; delta_v (d) receives the sum of
- * the replicas (zeroed by the call). */
+ * col_dot / col_axpy of dataset.py:77-78,90-91.  One warp per worker.  The
+ * private replicas live in dv_work (n_workers x d 64-bit words, zero-filled
+ * once at allocation): each word is (tag << 32 | fp32 bits) and reads as 0
+ * unless its tag is the running partition's, so replicas never need
+ * re-zeroing.  Partition p of a call uses tag replica_tag + p: the caller
+ * advances replica_tag by n_parts per call (skipping 0; a wrap of the 32-bit
+ * tag space needs a re-zero).  delta_v (d) receives the sum of the replicas
+ * (zeroed by the call). */
 typedef struct {
   int32_t kind;
   int64_t d;
@@ -160,10 +164,11 @@ typedef struct {
   int32_t n_parts;
   double a, lam, n_coords;
   int32_t iid;
-  float* dv_work;
+  uint64_t* dv_work;
   int32_t n_workers;
   float* delta_v;
   int32_t* status;
+  uint32_t replica_tag;
 } syscd_sparse_epoch_args;
 
 int syscd_sparse_epoch_workers(int64_t d, int32_t n_parts, int32_t* n_workers);

@@ -47,6 +47,7 @@ class SparseEpochArgs(ctypes.Structure):
         ("sq", c_vp), ("alpha", c_vp), ("u", c_vp), ("seq", c_vp), ("work_prefix", c_vp),
         ("n_parts", c_i32), ("a", c_f64), ("lam", c_f64), ("n_coords", c_f64), ("iid", c_i32),
         ("dv_work", c_vp), ("n_workers", c_i32), ("delta_v", c_vp), ("status", c_vp),
+        ("replica_tag", ctypes.c_uint32),
     ]
 
 

@@ -4,8 +4,10 @@
 //
 // B200 mapping.  One warp is one worker; a worker runs whole partitions in
 // sequence (contiguous, update-balanced ranges like the dense kernels).  The
-// private replica dv of the running partition is a dense fp32 d-vector in HBM
-// that is all-zero between partitions.
+// private replica dv of the running partition is a d-vector of tagged 64-bit
+// words in HBM, (tag << 32 | fp32): a word whose tag is not the running
+// partition's reads as zero, so a new partition starts from an all-zero
+// replica without any re-zeroing pass.
 //
 // The chain is processed in chunks of up to 32 consecutive updates holding at
 // most kChunkNnz nonzeros.  The chunk's rows are hashed into a shared-memory
@@ -21,8 +23,6 @@
 // the private replica and acc into the node sum (red.global.add).  Global
 // round trips drop from ~3 per update to ~3 per chunk.  A column longer than
 // the chunk capacity is processed on its own with lanes streaming it.
-// At a partition end the replica's touched rows are re-zeroed (lanes walk
-// different columns in parallel).
 //
 // The node sum uses fp32 atomics across workers, so this kernel is
 // deterministic only up to that summation order (documented in DESIGN.md).
@@ -47,9 +47,11 @@ struct SparseArgs {
   float lam_f, inv_n_f;
   double a_d, lam, n_coords;
   int32_t kind, iid;
-  float* dv_work;
+  unsigned long long* dv_work;  // tagged replicas (see syscd_b200.h)
   float* delta_v;
   int32_t* status;
+  uint32_t tag0;
+  unsigned long long* prof;  // debug: per-worker phase cycles (nullptr = off)
 };
 
 constexpr int kChunkNnz = 1024;  // nonzeros per chunk
@@ -66,6 +68,7 @@ struct SparseWarpSmem {
   float val[kChunkNnz];
   int row[kChunkNnz];
   float alpha_c[32];
+  float q_c[32];
   int col_j[32];
   int col_pre[33];
 };
@@ -87,6 +90,16 @@ __device__ __forceinline__ unsigned hash_row(int r) {
   return ((unsigned)r * 2654435761u) >> (32 - 11);  // 11 bits = kTable
 }
 
+// tagged replica word: (tag << 32) | fp32 bits; other tags read as zero
+__device__ __forceinline__ float rep_load(const unsigned long long* dv, int64_t r, uint32_t tag) {
+  const unsigned long long x = dv[r];
+  return (uint32_t)(x >> 32) == tag ? __uint_as_float((uint32_t)x) : 0.f;
+}
+
+__device__ __forceinline__ void rep_store(unsigned long long* dv, int64_t r, uint32_t tag, float v) {
+  dv[r] = ((unsigned long long)tag << 32) | __float_as_uint(v);
+}
+
 __device__ __forceinline__ float sparse_step(const SparseArgs& A, float lin, float aj, float qj) {
   if (A.kind == SYSCD_LOGISTIC_DUAL)
     return (float)coord_step(A.kind, (double)lin, A.a_d, (double)qj, A.lam, (double)aj,
@@ -106,13 +119,22 @@ __global__ void __launch_bounds__(32 * kSparseWarps) k_sparse_epoch(SparseArgs A
   const int64_t t_hi = (int64_t)((__int128)total * (g + 1) / W);
   const int64_t p_lo = g == 0 ? 0 : lb_i64(A.wp, A.n_parts + 1, t_lo);
   const int64_t p_hi = g == W - 1 ? A.n_parts : lb_i64(A.wp, A.n_parts + 1, t_hi);
-  float* dv = A.dv_work + (int64_t)g * A.d;
+  unsigned long long* dv = A.dv_work + (int64_t)g * A.d;
   const float a = A.a;
   for (int k = lane; k < kTable; k += 32) S.key[k] = kEmpty;
   __syncwarp();
+  unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tq = clock64();
+#define SPARSE_PHASE(i)                   \
+  if (A.prof) {                           \
+    const long long tn = clock64();       \
+    ph[i] += (unsigned long long)(tn - tq); \
+    tq = tn;                              \
+  }
 
   for (int64_t p = p_lo; p < p_hi; ++p) {
     const int64_t s0 = A.wp[p], s1 = A.wp[p + 1];
+    const uint32_t tag = A.tag0 + (uint32_t)p;
     int64_t c0 = s0;
     while (c0 < s1) {
       // ---- form the chunk: up to 32 columns with <= kChunkNnz nonzeros
@@ -133,6 +155,7 @@ __global__ void __launch_bounds__(32 * kSparseWarps) k_sparse_epoch(SparseArgs A
       }
       const unsigned fits = __ballot_sync(0xffffffffu, sl < s1 && pre <= kChunkNnz);
       const int m = __popc(fits);  // fits is a prefix of lanes
+      SPARSE_PHASE(0);
       if (m == 0) {
         // ---- a single long column: lanes stream it (no table)
         const int jj = __shfl_sync(0xffffffffu, j, 0);
@@ -140,7 +163,7 @@ __global__ void __launch_bounds__(32 * kSparseWarps) k_sparse_epoch(SparseArgs A
         float part = 0.f;
         for (int64_t e = a0 + lane; e < a1; e += 32) {
           const int i = A.ri[e];
-          part = fmaf(A.vals[e], fmaf(a, dv[i], A.u[i]), part);
+          part = fmaf(A.vals[e], fmaf(a, rep_load(dv, i, tag), A.u[i]), part);
         }
         part = warp_sum(part);
         const float aj = A.iid ? *(volatile float*)(A.alpha + jj) : A.alpha[jj];
@@ -156,12 +179,13 @@ __global__ void __launch_bounds__(32 * kSparseWarps) k_sparse_epoch(SparseArgs A
           for (int64_t e = a0 + lane; e < a1; e += 32) {
             const int i = A.ri[e];
             const float c = delta * A.vals[e];
-            dv[i] += c;
+            rep_store(dv, i, tag, rep_load(dv, i, tag) + c);
             red_add_f32(A.delta_v + i, c);
           }
         }
         __syncwarp();
         c0 += 1;
+        SPARSE_PHASE(7);
         continue;
       }
       // ---- stage the chunk's nonzeros and hash their rows (the table is
@@ -170,6 +194,7 @@ __global__ void __launch_bounds__(32 * kSparseWarps) k_sparse_epoch(SparseArgs A
         S.col_j[lane] = j;
         S.col_pre[lane + 1] = pre;
         S.alpha_c[lane] = A.iid ? *(volatile float*)(A.alpha + j) : A.alpha[j];
+        S.q_c[lane] = __ldg(A.sq + j);
       }
       if (lane == 0) S.col_pre[0] = 0;
       __syncwarp();
@@ -225,27 +250,42 @@ __global__ void __launch_bounds__(32 * kSparseWarps) k_sparse_epoch(SparseArgs A
         }
       }
       __syncwarp();
+      SPARSE_PHASE(1);
       // insert rows (each lane owns entries lane + 32k); owners of new slots
       // then gather b = u + a dv, 8 loads in flight per batch
+      // 8 first-probe CASes in flight per lane, collisions then probe on
       unsigned own = 0;
-      for (int k = 0; k < 32; ++k) {
-        const int e = lane + 32 * k;
-        if (e >= nz) break;
-        const int r = S.row[e];
-        unsigned h = hash_row(r);
-        while (true) {
-          const int prev = atomicCAS(&S.key[h], kEmpty, r);
-          if (prev == kEmpty) {
-            own |= 1u << k;
-            break;
-          }
-          if (prev == r) break;
-          h = (h + 1) & (kTable - 1);
-        }
-        S.slot[e] = (short)h;
-      }
       for (int k0 = 0; k0 < 32 && 32 * k0 < nz; k0 += 8) {
-        float uu[8], dd[8];
+        int rq[8], pq[8];
+        unsigned hq[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int e = lane + 32 * (k0 + q);
+          rq[q] = e < nz ? S.row[e] : kEmpty;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          hq[q] = hash_row(rq[q]);
+          pq[q] = rq[q] != kEmpty ? atomicCAS(&S.key[hq[q]], kEmpty, rq[q]) : kEmpty;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int e = lane + 32 * (k0 + q);
+          if (rq[q] == kEmpty) continue;
+          unsigned h = hq[q];
+          int prev = pq[q];
+          while (prev != kEmpty && prev != rq[q]) {
+            h = (h + 1) & (kTable - 1);
+            prev = atomicCAS(&S.key[h], kEmpty, rq[q]);
+          }
+          if (prev == kEmpty) own |= 1u << (k0 + q);
+          S.slot[e] = (short)h;
+        }
+      }
+      SPARSE_PHASE(2);
+      for (int k0 = 0; k0 < 32 && 32 * k0 < nz; k0 += 8) {
+        float uu[8];
+        unsigned long long dw[8];  // raw tagged words: decoded after all loads issue
         int hh[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -256,19 +296,21 @@ __global__ void __launch_bounds__(32 * kSparseWarps) k_sparse_epoch(SparseArgs A
             const int r = S.row[e];
             hh[q] = S.slot[e];
             uu[q] = A.u[r];
-            dd[q] = dv[r];
+            dw[q] = dv[r];
           }
         }
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           if (hh[q] >= 0) {
-            S.dvold[hh[q]] = dd[q];
-            S.b[hh[q]] = fmaf(a, dd[q], uu[q]);
+            const float dd = (uint32_t)(dw[q] >> 32) == tag ? __uint_as_float((uint32_t)dw[q]) : 0.f;
+            S.dvold[hh[q]] = dd;
+            S.b[hh[q]] = fmaf(a, dd, uu[q]);
             S.acc[hh[q]] = 0.f;
           }
         }
       }
       __syncwarp();
+      SPARSE_PHASE(3);
       // ---- the chain, entirely in shared memory
       for (int t = 0; t < m; ++t) {
         const int b0 = S.col_pre[t], b1 = S.col_pre[t + 1];
@@ -277,7 +319,7 @@ __global__ void __launch_bounds__(32 * kSparseWarps) k_sparse_epoch(SparseArgs A
         const float lin = warp_sum(part);
         const int jt = S.col_j[t];
         const float aj = S.alpha_c[t];
-        const float an = sparse_step(A, lin, aj, __ldg(A.sq + jt));
+        const float an = sparse_step(A, lin, aj, S.q_c[t]);
         float delta = 0.f;
         if (isfinite(an)) {
           delta = an - aj;
@@ -298,32 +340,32 @@ __global__ void __launch_bounds__(32 * kSparseWarps) k_sparse_epoch(SparseArgs A
         if (lane == 0 && isfinite(an)) A.alpha[jt] = aj + delta;
         __syncwarp();
       }
+      SPARSE_PHASE(4);
       // ---- write back every distinct row once (by the lane that inserted
       // it) and release its slot
       for (unsigned o = own; o; o &= o - 1) {
         const int e = lane + 32 * (__ffs(o) - 1);
         const int h = S.slot[e];
         const int r = S.row[e];
-        const float c = S.acc[h];
-        if (c != 0.f) {
-          dv[r] = S.dvold[h] + c;
-          red_add_f32(A.delta_v + r, c);
+        const float cv = S.acc[h];
+        if (cv != 0.f) {
+          rep_store(dv, r, tag, S.dvold[h] + cv);
+          red_add_f32(A.delta_v + r, cv);
         }
         S.key[h] = kEmpty;
       }
       __syncwarp();
       c0 += m;
+      SPARSE_PHASE(5);
     }
-    // restore the all-zero replica: lanes walk different columns in parallel
-    // (a row shared by two columns is simply zeroed twice)
-    for (int64_t s = s0 + lane; s < s1; s += 32) {
-      const int jj = A.seq[s];
-      const int64_t q0 = A.cp[jj], q1 = A.cp[jj + 1];
-      for (int64_t e = q0; e < q1; ++e) dv[A.ri[e]] = 0.f;
-    }
-    __syncwarp();
+    SPARSE_PHASE(6);
   }
+#undef SPARSE_PHASE
+  if (A.prof && lane == 0)
+    for (int i = 0; i < 8; ++i) A.prof[(int64_t)g * 8 + i] = ph[i];
 }
+
+static unsigned long long* g_sparse_prof = nullptr;
 
 static int sparse_workers(int32_t n_parts) {
   int dev = 0, sms = 148;
@@ -335,6 +377,14 @@ static int sparse_workers(int32_t n_parts) {
 }  // namespace syscd
 
 using namespace syscd;
+
+// Debug hook (not part of the C-ABI contract): with a device buffer of
+// n_workers * 8 uint64, the next sparse epochs record per-worker cycles spent
+// in: chunk formation, column copy, hash insert, gather, chain, writeback,
+// partition-end zeroing, long-column path.
+extern "C" void syscd_debug_set_sparse_profile(void* device_buffer) {
+  g_sparse_prof = (unsigned long long*)device_buffer;
+}
 
 extern "C" int syscd_sparse_epoch_workers(int64_t d, int32_t n_parts, int32_t* n_workers) {
   if (d < 1 || n_parts < 1 || !n_workers) {
@@ -372,9 +422,11 @@ extern "C" int syscd_sparse_epoch(const syscd_sparse_epoch_args* e, void* stream
   A.n_coords = e->n_coords;
   A.kind = e->kind;
   A.iid = e->iid;
-  A.dv_work = e->dv_work;
+  A.dv_work = (unsigned long long*)e->dv_work;
+  A.tag0 = e->replica_tag;
   A.delta_v = e->delta_v;
   A.status = e->status;
+  A.prof = g_sparse_prof;
   cudaStream_t s = (cudaStream_t)stream;
   SYSCD_CUDA_TRY(cudaMemsetAsync(e->delta_v, 0, e->d * sizeof(float), s));
   const size_t smem = sizeof(SparseWarpSmem) * kSparseWarps;

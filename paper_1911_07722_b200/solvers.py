@@ -210,7 +210,9 @@ class _Engine:
             call("syscd_sparse_epoch_workers", d, self.n_parts_local, ctypes.byref(nw))
             self.n_workers = nw.value
             self.cluster = 1
-            self.dv_work = torch.zeros(self.n_workers * d, dtype=torch.float32, device="cuda")
+            # tagged replica words (tag << 32 | fp32), zero-filled once
+            self.dv_work = torch.zeros(self.n_workers * d, dtype=torch.int64, device="cuda")
+            self.replica_tag = 1
             self.part_ld = d
             self.partials = torch.empty(d, dtype=torch.float32, device="cuda")
         self.alpha = torch.zeros(dp.n_store, dtype=torch.float32, device="cuda")
@@ -331,6 +333,11 @@ class _Engine:
             e.n_coords = dp.n_coords
             e.iid = 1 if cfg.sampling == "iid" else 0
             e.dv_work = self.dv_work.data_ptr()
+            if self.replica_tag + nparts >= 1 << 32:  # tag space wrapped: re-zero
+                self.dv_work.zero_()
+                self.replica_tag = 1
+            e.replica_tag = self.replica_tag
+            self.replica_tag += nparts
             e.n_workers = self.n_workers
             e.delta_v = self.dv.data_ptr()
             e.status = self.status.data_ptr()
