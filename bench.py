@@ -233,7 +233,7 @@ def run_ours(args):
         "epochs_per_s": 1e3 / ms_per_step,
         "roofline": {
             "bound": "hbm",
-            "kernel": "k_dense_epoch" if dp.storage == "dense" else "k_sparse_epoch",
+            "kernel": _epoch_kernel_name(dp, eng),
             "achieved": achieved,
             "peak": hbm,
             "peak_source": peak_kind,
@@ -257,6 +257,18 @@ def run_ours(args):
         print(json.dumps(out), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def _epoch_kernel_name(dp, eng):
+    """Which epoch kernel syscd_dense_epoch / syscd_sparse_epoch dispatches to."""
+    from paper_1911_07722_b200._lib import lib
+    if dp.storage != "dense":
+        return "k_sparse_epoch"
+    if dp.d <= 32:
+        return "k_small_epoch"
+    if int(lib().syscd_dense_epoch_workspace_bytes(dp.d, eng.n_parts_local)) > 0:
+        return "k_grid_epoch"
+    return "k_dense_epoch"
 
 
 def time_to_target(wl, args, target=1e-4, max_epochs=2000):
