@@ -2,27 +2,32 @@
 // (dataset.py:77-78, 90-91) inside _surrogate_thread_round
 // (solvers.py:289-334).
 //
-// B200 mapping.  One warp is one worker; a worker runs whole partitions in
-// sequence (contiguous, update-balanced ranges like the dense kernels).  The
-// private replica dv of the running partition is a d-vector of tagged 64-bit
-// words in HBM, (tag << 32 | fp32): a word whose tag is not the running
-// partition's reads as zero, so a new partition starts from an all-zero
-// replica without any re-zeroing pass.
+// B200 mapping.  A worker (one 64-thread block = a consumer warp and a
+// producer warp) runs whole partitions in sequence (contiguous,
+// update-balanced ranges like the dense kernels).  The private replica dv of
+// the running partition is a d-vector of tagged 64-bit words in HBM,
+// (tag << 32 | fp32): a word whose tag is not the running partition's reads as
+// zero, so a new partition starts from an all-zero replica without any
+// re-zeroing pass.
 //
-// The chain is processed in chunks of up to 32 consecutive updates holding at
-// most kChunkNnz nonzeros.  The chunk's rows are hashed into a shared-memory
-// table (one slot per distinct row) that holds b = u + a dv for that row and
-// the chunk's accumulated replica change; every update then runs entirely in
-// shared memory:
+// The chain is cut into chunks of up to 32 consecutive updates holding at most
+// kPcNnz nonzeros.  The producer stages a chunk into one of two shared-memory
+// buffers: the columns' rows and values, a hash table with one slot per
+// distinct row (linear probing, the inserting lane owns the slot), and per
+// slot b = u + a dv gathered once.  The consumer then runs the chain entirely
+// in shared memory:
 //     lin_t = sum_{e in col t} val_e * b[slot_e]        (lanes over nonzeros)
-//     alpha_t <- step(lin_t)                             (fp64 for logistic dual)
+//     alpha_t <- step(lin_t)
 //     b[slot_e] += a delta_t val_e ; acc[slot_e] += delta_t val_e
 // which is exactly the reference's per-coordinate chain (rows shared by two
-// columns of the chunk see each other's updates through the shared slot).  At
-// the chunk end every distinct row is written back once: dv = dv_old + acc in
-// the private replica and acc into the node sum (red.global.add).  Global
-// round trips drop from ~3 per update to ~3 per chunk.  A column longer than
-// the chunk capacity is processed on its own with lanes streaming it.
+// columns of the chunk see each other's updates through the shared slot).
+// While chunk k's chain runs, the producer writes back chunk k-1's buffer
+// (dv = dv_old + acc per distinct row, acc into the node sum with
+// red.global.add) and stages chunk k+1.  Chunk k+1 was gathered before chunk
+// k's updates reached memory, so after its chain the consumer patches chunk
+// k+1's copy of every row chunk k changed (a hash probe; both tables use the
+// same hash, so most probes hit the first slot).  A column longer than the
+// chunk capacity is streamed by the consumer on its own.
 //
 // The node sum uses fp32 atomics across workers, so this kernel is
 // deterministic only up to that summation order (documented in DESIGN.md).
@@ -54,24 +59,7 @@ struct SparseArgs {
   unsigned long long* prof;  // debug: per-worker phase cycles (nullptr = off)
 };
 
-constexpr int kChunkNnz = 1024;  // nonzeros per chunk
-constexpr int kTable = 2048;     // hash slots (>= 2 x kChunkNnz)
-constexpr int kSparseWarps = 4;  // workers per block
 constexpr int kEmpty = -1;
-
-struct SparseWarpSmem {
-  int key[kTable];
-  float b[kTable];
-  float acc[kTable];
-  float dvold[kTable];
-  short slot[kChunkNnz];
-  float val[kChunkNnz];
-  int row[kChunkNnz];
-  float alpha_c[32];
-  float q_c[32];
-  int col_j[32];
-  int col_pre[33];
-};
 
 __device__ __forceinline__ int64_t lb_i64(const int64_t* a, int n, int64_t key) {
   int lo = 0, hi = n;
@@ -86,13 +74,14 @@ __device__ __forceinline__ int64_t lb_i64(const int64_t* a, int n, int64_t key) 
   return lo;
 }
 
-__device__ __forceinline__ unsigned hash_row(int r) {
-  return ((unsigned)r * 2654435761u) >> (32 - 11);  // 11 bits = kTable
-}
-
 // tagged replica word: (tag << 32) | fp32 bits; other tags read as zero
 __device__ __forceinline__ float rep_load(const unsigned long long* dv, int64_t r, uint32_t tag) {
   const unsigned long long x = dv[r];
+  return (uint32_t)(x >> 32) == tag ? __uint_as_float((uint32_t)x) : 0.f;
+}
+
+__device__ __forceinline__ float rep_load_cg(const unsigned long long* dv, int64_t r, uint32_t tag) {
+  const unsigned long long x = __ldcg(dv + r);
   return (uint32_t)(x >> 32) == tag ? __uint_as_float((uint32_t)x) : 0.f;
 }
 
@@ -107,13 +96,243 @@ __device__ __forceinline__ float sparse_step(const SparseArgs& A, float lin, flo
   return coord_step_f(A.kind, lin, A.a, qj, A.lam_f, aj, A.inv_n_f);
 }
 
-__global__ void __launch_bounds__(32 * kSparseWarps) k_sparse_epoch(SparseArgs A, int W) {
+constexpr int kPcNnz = 512;
+constexpr int kPcTable = 1024;
+
+struct PcBuf {
+  int key[kPcTable];
+  float b[kPcTable];
+  float acc[kPcTable];
+  float dvold[kPcTable];
+  short slot[kPcNnz];
+  short uniq[kPcNnz];  // the chunk's distinct slots
+  float val[kPcNnz];
+  int row[kPcNnz];
+  float alpha_c[32];
+  float q_c[32];
+  int col_j[32];
+  int col_pre[33];
+  int m;  // columns; 0 = one long column (col_j[0]); -1 = end of the worker's work
+  int n_uniq;
+  uint32_t tag;
+};
+
+struct PcSmem {
+  PcBuf buf[2];
+  uint64_t full[2];
+  uint64_t empty[2];
+};
+
+__device__ __forceinline__ unsigned pc_hash(int r) {
+  return ((unsigned)r * 2654435761u) >> (32 - 10);  // 10 bits = kPcTable
+}
+
+__device__ __forceinline__ int pc_find(const PcBuf& T, int r) {
+  unsigned h = pc_hash(r);
+  int k;
+  while ((k = T.key[h]) != kEmpty) {
+    if (k == r) return (int)h;
+    h = (h + 1) & (kPcTable - 1);
+  }
+  return -1;
+}
+
+// Stage the chunk starting at c0 of the partition into B.
+__device__ __forceinline__ void pc_produce(const SparseArgs& A, PcBuf& B, int lane, int64_t c0,
+                                           int64_t s1, uint32_t tag,
+                                           const unsigned long long* dv, int* m_out) {
+  const float a = A.a;
+  const int64_t sl = c0 + lane;
+  int j = 0, nnz = 0;
+  int64_t e0 = 0;
+  if (sl < s1) {
+    j = A.seq[sl];
+    e0 = A.cp[j];
+    nnz = (int)(A.cp[j + 1] - e0);
+  }
+  int pre = nnz;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, pre, o);
+    if (lane >= o) pre += v;
+  }
+  const unsigned fits = __ballot_sync(0xffffffffu, sl < s1 && pre <= kPcNnz);
+  const int m = __popc(fits);
+  *m_out = m;
+  if (lane == 0) B.tag = tag;
+  if (m == 0) {  // one long column: the consumer streams it from global memory
+    if (lane == 0) {
+      B.m = 0;
+      B.col_j[0] = j;
+    }
+    return;
+  }
+  if (lane < m) {
+    B.col_j[lane] = j;
+    B.col_pre[lane + 1] = pre;
+    if (!A.iid) B.alpha_c[lane] = A.alpha[j];
+    B.q_c[lane] = __ldg(A.sq + j);
+  }
+  if (lane == 0) {
+    B.col_pre[0] = 0;
+    B.m = m;
+  }
+
+  const int nz = __shfl_sync(0xffffffffu, pre, m - 1);
+  // copy: all lanes on one column, 8 columns' loads in flight
+  for (int t0 = 0; t0 < m; t0 += 8) {
+    int rr[8][2];
+    float vv[8][2];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int t = t0 + q;
+      const int64_t et = __shfl_sync(0xffffffffu, e0, t & 31);
+      const int nt = __shfl_sync(0xffffffffu, nnz, t & 31);
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int k = lane + 32 * h2;
+        if (t < m && k < nt) {
+          rr[q][h2] = __ldg(A.ri + et + k);
+          vv[q][h2] = __ldg(A.vals + et + k);
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int t = t0 + q;
+      const int nt = __shfl_sync(0xffffffffu, nnz, t & 31);
+      const int bt = __shfl_sync(0xffffffffu, pre - nnz, t & 31);
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int k = lane + 32 * h2;
+        if (t < m && k < nt) {
+          B.row[bt + k] = rr[q][h2];
+          B.val[bt + k] = vv[q][h2];
+        }
+      }
+    }
+#pragma unroll 1
+    for (int q = 0; q < 8; ++q) {
+      const int t = t0 + q;
+      const int nt = __shfl_sync(0xffffffffu, nnz, t & 31);
+      const int64_t et = __shfl_sync(0xffffffffu, e0, t & 31);
+      const int bt = __shfl_sync(0xffffffffu, pre - nnz, t & 31);
+      if (t < m && nt > 64)
+        for (int k = 64 + lane; k < nt; k += 32) {
+          B.row[bt + k] = __ldg(A.ri + et + k);
+          B.val[bt + k] = __ldg(A.vals + et + k);
+        }
+    }
+  }
+  __syncwarp();
+  // insert: 8 first-probe CASes in flight per lane; the inserting lane owns
+  // the slot
+  unsigned own = 0;
+  for (int k0 = 0; k0 < kPcNnz / 32 && 32 * k0 < nz; k0 += 8) {
+    int rq[8], pq[8];
+    unsigned hq[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = lane + 32 * (k0 + q);
+      rq[q] = e < nz ? B.row[e] : kEmpty;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      hq[q] = pc_hash(rq[q]);
+      pq[q] = rq[q] != kEmpty ? atomicCAS(&B.key[hq[q]], kEmpty, rq[q]) : kEmpty;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = lane + 32 * (k0 + q);
+      if (rq[q] == kEmpty) continue;
+      unsigned h = hq[q];
+      int prev = pq[q];
+      while (prev != kEmpty && prev != rq[q]) {
+        h = (h + 1) & (kPcTable - 1);
+        prev = atomicCAS(&B.key[h], kEmpty, rq[q]);
+      }
+      if (prev == kEmpty) own |= 1u << (k0 + q);
+      B.slot[e] = (short)h;
+    }
+  }
+  // distinct-slot list (warp prefix over the owners' counts)
+  const int cnt = __popc(own);
+  int base = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, base, o);
+    if (lane >= o) base += v;
+  }
+  if (lane == 31) B.n_uniq = base;
+  base -= cnt;
+  // gather u and the replica for owned slots (8 loads in flight; the
+  // replica through L2: the consumer warp writes it)
+  for (int k0 = 0; k0 < kPcNnz / 32 && 32 * k0 < nz; k0 += 8) {
+    float uu[8];
+    unsigned long long dw[8];
+    int hh[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int k = k0 + q;
+      hh[q] = -1;
+      if ((own >> k) & 1u) {
+        const int e = lane + 32 * k;
+        const int r = B.row[e];
+        hh[q] = B.slot[e];
+        uu[q] = __ldg(A.u + r);
+        dw[q] = __ldcg(dv + r);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (hh[q] >= 0) {
+        const float dd =
+            (uint32_t)(dw[q] >> 32) == tag ? __uint_as_float((uint32_t)dw[q]) : 0.f;
+        B.dvold[hh[q]] = dd;
+        B.b[hh[q]] = fmaf(a, dd, uu[q]);
+        B.acc[hh[q]] = 0.f;
+        B.uniq[base++] = (short)hh[q];
+
+      }
+    }
+  }
+}
+
+// patch the next buffer's copy of row r (gathered before this writeback)
+__device__ __forceinline__ void pc_patch(PcBuf& N, int r, float nv, float a) {
+  unsigned h = pc_hash(r);
+  int k;
+  while ((k = N.key[h]) != kEmpty) {
+    if (k == r) {
+      N.b[h] = fmaf(a, nv - N.dvold[h], N.b[h]);
+      N.dvold[h] = nv;
+      return;
+    }
+    h = (h + 1) & (kPcTable - 1);
+  }
+}
+
+__global__ void __launch_bounds__(64) k_sparse_epoch(SparseArgs A, int W) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  PcSmem& S = *reinterpret_cast<PcSmem*>(smem_raw);
   const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  const int g = blockIdx.x * kSparseWarps + wib;
+  const int warp = threadIdx.x >> 5;
+  const int g = blockIdx.x;
   if (g >= W) return;
-  SparseWarpSmem& S = reinterpret_cast<SparseWarpSmem*>(smem_raw)[wib];
+  for (int k = threadIdx.x; k < kPcTable; k += 64) {
+    S.buf[0].key[k] = kEmpty;
+    S.buf[1].key[k] = kEmpty;
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&S.full[i], 1);
+      mbar_init(&S.empty[i], 1);
+      S.buf[i].m = -1;
+      S.buf[i].tag = 0;
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
   const int64_t total = A.wp[A.n_parts];
   const int64_t t_lo = (int64_t)((__int128)total * g / W);
   const int64_t t_hi = (int64_t)((__int128)total * (g + 1) / W);
@@ -121,52 +340,96 @@ __global__ void __launch_bounds__(32 * kSparseWarps) k_sparse_epoch(SparseArgs A
   const int64_t p_hi = g == W - 1 ? A.n_parts : lb_i64(A.wp, A.n_parts + 1, t_hi);
   unsigned long long* dv = A.dv_work + (int64_t)g * A.d;
   const float a = A.a;
-  for (int k = lane; k < kTable; k += 32) S.key[k] = kEmpty;
-  __syncwarp();
-  unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long ph[4] = {0, 0, 0, 0};
   long long tq = clock64();
-#define SPARSE_PHASE(i)                   \
-  if (A.prof) {                           \
-    const long long tn = clock64();       \
+#define PC_PHASE(i)                         \
+  if (A.prof) {                             \
+    const long long tn = clock64();         \
     ph[i] += (unsigned long long)(tn - tq); \
-    tq = tn;                              \
+    tq = tn;                                \
   }
 
-  for (int64_t p = p_lo; p < p_hi; ++p) {
-    const int64_t s0 = A.wp[p], s1 = A.wp[p + 1];
-    const uint32_t tag = A.tag0 + (uint32_t)p;
-    int64_t c0 = s0;
-    while (c0 < s1) {
-      // ---- form the chunk: up to 32 columns with <= kChunkNnz nonzeros
-      const int64_t sl = c0 + lane;
-      int j = 0;
-      int nnz = 0;
-      int64_t e0 = 0;
-      if (sl < s1) {
-        j = A.seq[sl];
-        e0 = A.cp[j];
-        nnz = (int)(A.cp[j + 1] - e0);
+  if (warp == 1) {
+    // ---------------- producer ----------------
+    // chunk k goes to buffer k&1; before refilling a buffer the producer
+    // writes back the chunk it held (k-2): replica words and the node sum.
+    auto writeback = [&](PcBuf& B) {
+      if (B.m > 0) {
+        const uint32_t tag = B.tag;
+        const int nu = B.n_uniq;
+        for (int i = lane; i < nu; i += 32) {
+          const int h = B.uniq[i];
+          const int r = B.key[h];
+          const float cv = B.acc[h];
+          if (cv != 0.f) {
+            rep_store(dv, r, tag, B.dvold[h] + cv);
+            red_add_f32(A.delta_v + r, cv);
+          }
+          B.key[h] = kEmpty;
+        }
       }
-      int pre = nnz;  // inclusive scan
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, pre, o);
-        if (lane >= o) pre += v;
+      __syncwarp();
+    };
+    int k = 0;
+    for (int64_t p = p_lo; p <= p_hi; ++p) {
+      const bool end = p == p_hi;
+      const int64_t s0 = end ? 0 : A.wp[p], s1 = end ? 1 : A.wp[p + 1];
+      int64_t c0 = s0;
+      while (c0 < s1) {
+        const int bi = k & 1;
+        PcBuf& B = S.buf[bi];
+        if (k >= 2) {
+          mbar_wait(&S.empty[bi], ((k >> 1) - 1) & 1);
+          PC_PHASE(0);
+          writeback(B);
+          PC_PHASE(1);
+        }
+        int m = 1;
+        if (end) {
+          if (lane == 0) B.m = -1;
+        } else {
+          pc_produce(A, B, lane, c0, s1, A.tag0 + (uint32_t)p, dv, &m);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.full[bi]);
+        PC_PHASE(2);
+        c0 += m > 0 ? m : 1;
+        ++k;
       }
-      const unsigned fits = __ballot_sync(0xffffffffu, sl < s1 && pre <= kChunkNnz);
-      const int m = __popc(fits);  // fits is a prefix of lanes
-      SPARSE_PHASE(0);
+    }
+    // k-1 is the end marker; chunk k-2 still holds updates
+    if (k >= 2) {
+      const int bi = k & 1;  // == (k-2)&1
+      mbar_wait(&S.empty[bi], ((k >> 1) - 1) & 1);
+      writeback(S.buf[bi]);
+    }
+  } else {
+    // ---------------- consumer ----------------
+    for (int k = 0;; ++k) {
+      const int bi = k & 1;
+      mbar_wait(&S.full[bi], (k >> 1) & 1);
+      PcBuf& C = S.buf[bi];
+      const int m = C.m;
+      if (m < 0) break;
+      const uint32_t tag = C.tag;
+      const int nb = (k + 1) & 1;
+      PcBuf& N = S.buf[nb];
+      PC_PHASE(0);
       if (m == 0) {
-        // ---- a single long column: lanes stream it (no table)
-        const int jj = __shfl_sync(0xffffffffu, j, 0);
+        // a single long column, streamed with the replica read and written in
+        // place.  Chunk k+1 being staged means the producer has written back
+        // chunk k-1, so the replica in memory is current.
+        mbar_wait(&S.full[nb], ((k + 1) >> 1) & 1);
+        const bool patch = N.m > 0 && N.tag == tag;
+        const int jj = C.col_j[0];
         const int64_t a0 = A.cp[jj], a1 = A.cp[jj + 1];
         float part = 0.f;
         for (int64_t e = a0 + lane; e < a1; e += 32) {
           const int i = A.ri[e];
-          part = fmaf(A.vals[e], fmaf(a, rep_load(dv, i, tag), A.u[i]), part);
+          part = fmaf(A.vals[e], fmaf(a, rep_load_cg(dv, i, tag), A.u[i]), part);
         }
         part = warp_sum(part);
-        const float aj = A.iid ? *(volatile float*)(A.alpha + jj) : A.alpha[jj];
+        const float aj = *(volatile float*)(A.alpha + jj);
         const float an = sparse_step(A, part, aj, __ldg(A.sq + jj));
         float delta = 0.f;
         if (isfinite(an)) {
@@ -179,199 +442,106 @@ __global__ void __launch_bounds__(32 * kSparseWarps) k_sparse_epoch(SparseArgs A
           for (int64_t e = a0 + lane; e < a1; e += 32) {
             const int i = A.ri[e];
             const float c = delta * A.vals[e];
-            rep_store(dv, i, tag, rep_load(dv, i, tag) + c);
+            const float nv = rep_load_cg(dv, i, tag) + c;
+            rep_store(dv, i, tag, nv);
             red_add_f32(A.delta_v + i, c);
+            if (patch) pc_patch(N, i, nv, a);
           }
         }
         __syncwarp();
-        c0 += 1;
-        SPARSE_PHASE(7);
-        continue;
-      }
-      // ---- stage the chunk's nonzeros and hash their rows (the table is
-      // empty here: cleared once at start, used slots reset at writeback)
-      if (lane < m) {
-        S.col_j[lane] = j;
-        S.col_pre[lane + 1] = pre;
-        S.alpha_c[lane] = A.iid ? *(volatile float*)(A.alpha + j) : A.alpha[j];
-        S.q_c[lane] = __ldg(A.sq + j);
-      }
-      if (lane == 0) S.col_pre[0] = 0;
-      __syncwarp();
-      const int nz = S.col_pre[m];
-      // copy the chunk's nonzeros: all lanes on one column, 8 columns' loads
-      // in flight before their shared-memory stores
-      for (int t0 = 0; t0 < m; t0 += 8) {
-        int rr[8][2];
-        float vv[8][2];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int t = t0 + q;
-          const int jt = __shfl_sync(0xffffffffu, j, t & 31);
-          const int64_t et = __shfl_sync(0xffffffffu, e0, t & 31);
-          const int nt = __shfl_sync(0xffffffffu, nnz, t & 31);
-#pragma unroll
-          for (int h2 = 0; h2 < 2; ++h2) {
-            const int k = lane + 32 * h2;
-            if (t < m && k < nt) {
-              rr[q][h2] = A.ri[et + k];
-              vv[q][h2] = A.vals[et + k];
+        PC_PHASE(1);
+      } else {
+        if (A.iid && lane < m) C.alpha_c[lane] = *(volatile float*)(A.alpha + C.col_j[lane]);
+        __syncwarp();
+        for (int t = 0; t < m; ++t) {
+          const int b0 = C.col_pre[t], b1 = C.col_pre[t + 1];
+          float part = 0.f;
+          for (int e = b0 + lane; e < b1; e += 32) part = fmaf(C.val[e], C.b[C.slot[e]], part);
+          const float lin = warp_sum(part);
+          const int jt = C.col_j[t];
+          const float aj = C.alpha_c[t];
+          const float an = sparse_step(A, lin, aj, C.q_c[t]);
+          float delta = 0.f;
+          if (isfinite(an)) {
+            delta = an - aj;
+          } else if (lane == 0) {
+            atomicOr(A.status, SYSCD_ENONFINITE);
+          }
+          if (delta != 0.f) {
+            for (int e = b0 + lane; e < b1; e += 32) {
+              const int h = C.slot[e];
+              const float c = delta * C.val[e];
+              C.b[h] = fmaf(a, c, C.b[h]);
+              C.acc[h] += c;
             }
           }
-          (void)jt;
+          if (lane < m && lane > t && C.col_j[lane] == jt) C.alpha_c[lane] = aj + delta;
+          if (lane == 0 && isfinite(an)) A.alpha[jt] = aj + delta;
+          __syncwarp();
         }
+        PC_PHASE(1);
+        // chunk k+1 was staged from the replica before this chunk's updates
+        // reach memory: patch its copy of every row written here
+        mbar_wait(&S.full[nb], ((k + 1) >> 1) & 1);
+        PC_PHASE(2);
+        if (N.m > 0 && N.tag == tag) {
+          // both tables use the same hash, so most rows sit at their first
+          // probe position: 4 rows' probes in flight per lane
+          const int nu = C.n_uniq;
+          for (int i0 = lane; i0 < nu; i0 += 128) {
+            int rq[4], kq[4];
+            unsigned hq[4];
+            float nvq[4];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int t = t0 + q;
-          const int nt = __shfl_sync(0xffffffffu, nnz, t & 31);
-          const int bt = __shfl_sync(0xffffffffu, pre - nnz, t & 31);
+            for (int q = 0; q < 4; ++q) {
+              const int i = i0 + 32 * q;
+              rq[q] = kEmpty;
+              if (i < nu) {
+                const int h = C.uniq[i];
+                const float cv = C.acc[h];
+                if (cv != 0.f) {
+                  rq[q] = C.key[h];
+                  nvq[q] = C.dvold[h] + cv;
+                }
+              }
+              hq[q] = pc_hash(rq[q]);
+              kq[q] = rq[q] != kEmpty ? N.key[hq[q]] : kEmpty;
+            }
 #pragma unroll
-          for (int h2 = 0; h2 < 2; ++h2) {
-            const int k = lane + 32 * h2;
-            if (t < m && k < nt) {
-              S.row[bt + k] = rr[q][h2];
-              S.val[bt + k] = vv[q][h2];
+            for (int q = 0; q < 4; ++q) {
+              if (kq[q] == kEmpty) continue;
+              int hn = kq[q] == rq[q] ? (int)hq[q] : pc_find(N, rq[q]);
+              if (hn >= 0) {
+                N.b[hn] = fmaf(a, nvq[q] - N.dvold[hn], N.b[hn]);
+                N.dvold[hn] = nvq[q];
+              }
             }
           }
         }
-        // columns longer than 64 nonzeros: the rest, plainly
-#pragma unroll 1
-        for (int q = 0; q < 8; ++q) {
-          const int t = t0 + q;
-          const int nt = __shfl_sync(0xffffffffu, nnz, t & 31);
-          const int64_t et = __shfl_sync(0xffffffffu, e0, t & 31);
-          const int bt = __shfl_sync(0xffffffffu, pre - nnz, t & 31);
-          if (t < m && nt > 64) {
-            for (int k = 64 + lane; k < nt; k += 32) {
-              S.row[bt + k] = A.ri[et + k];
-              S.val[bt + k] = A.vals[et + k];
-            }
-          }
-        }
-      }
-      __syncwarp();
-      SPARSE_PHASE(1);
-      // insert rows (each lane owns entries lane + 32k); owners of new slots
-      // then gather b = u + a dv, 8 loads in flight per batch
-      // 8 first-probe CASes in flight per lane, collisions then probe on
-      unsigned own = 0;
-      for (int k0 = 0; k0 < 32 && 32 * k0 < nz; k0 += 8) {
-        int rq[8], pq[8];
-        unsigned hq[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int e = lane + 32 * (k0 + q);
-          rq[q] = e < nz ? S.row[e] : kEmpty;
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          hq[q] = hash_row(rq[q]);
-          pq[q] = rq[q] != kEmpty ? atomicCAS(&S.key[hq[q]], kEmpty, rq[q]) : kEmpty;
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int e = lane + 32 * (k0 + q);
-          if (rq[q] == kEmpty) continue;
-          unsigned h = hq[q];
-          int prev = pq[q];
-          while (prev != kEmpty && prev != rq[q]) {
-            h = (h + 1) & (kTable - 1);
-            prev = atomicCAS(&S.key[h], kEmpty, rq[q]);
-          }
-          if (prev == kEmpty) own |= 1u << (k0 + q);
-          S.slot[e] = (short)h;
-        }
-      }
-      SPARSE_PHASE(2);
-      for (int k0 = 0; k0 < 32 && 32 * k0 < nz; k0 += 8) {
-        float uu[8];
-        unsigned long long dw[8];  // raw tagged words: decoded after all loads issue
-        int hh[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int k = k0 + q;
-          hh[q] = -1;
-          if ((own >> k) & 1u) {
-            const int e = lane + 32 * k;
-            const int r = S.row[e];
-            hh[q] = S.slot[e];
-            uu[q] = A.u[r];
-            dw[q] = dv[r];
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          if (hh[q] >= 0) {
-            const float dd = (uint32_t)(dw[q] >> 32) == tag ? __uint_as_float((uint32_t)dw[q]) : 0.f;
-            S.dvold[hh[q]] = dd;
-            S.b[hh[q]] = fmaf(a, dd, uu[q]);
-            S.acc[hh[q]] = 0.f;
-          }
-        }
-      }
-      __syncwarp();
-      SPARSE_PHASE(3);
-      // ---- the chain, entirely in shared memory
-      for (int t = 0; t < m; ++t) {
-        const int b0 = S.col_pre[t], b1 = S.col_pre[t + 1];
-        float part = 0.f;
-        for (int e = b0 + lane; e < b1; e += 32) part = fmaf(S.val[e], S.b[S.slot[e]], part);
-        const float lin = warp_sum(part);
-        const int jt = S.col_j[t];
-        const float aj = S.alpha_c[t];
-        const float an = sparse_step(A, lin, aj, S.q_c[t]);
-        float delta = 0.f;
-        if (isfinite(an)) {
-          delta = an - aj;
-        } else if (lane == 0) {
-          atomicOr(A.status, SYSCD_ENONFINITE);
-        }
-        if (delta != 0.f) {
-          for (int e = b0 + lane; e < b1; e += 32) {
-            const int h = S.slot[e];
-            const float c = delta * S.val[e];
-            S.b[h] = fmaf(a, c, S.b[h]);
-            S.acc[h] += c;
-          }
-        }
-        // later occurrences of the same coordinate (iid) see its new value
-        if (lane < m && lane > t && S.col_j[lane] == jt) S.alpha_c[lane] = aj + delta;
-        // the last occurrence's value is the one that survives
-        if (lane == 0 && isfinite(an)) A.alpha[jt] = aj + delta;
         __syncwarp();
       }
-      SPARSE_PHASE(4);
-      // ---- write back every distinct row once (by the lane that inserted
-      // it) and release its slot
-      for (unsigned o = own; o; o &= o - 1) {
-        const int e = lane + 32 * (__ffs(o) - 1);
-        const int h = S.slot[e];
-        const int r = S.row[e];
-        const float cv = S.acc[h];
-        if (cv != 0.f) {
-          rep_store(dv, r, tag, S.dvold[h] + cv);
-          red_add_f32(A.delta_v + r, cv);
-        }
-        S.key[h] = kEmpty;
-      }
-      __syncwarp();
-      c0 += m;
-      SPARSE_PHASE(5);
+      if (lane == 0) mbar_arrive(&S.empty[bi]);
+      PC_PHASE(3);
     }
-    SPARSE_PHASE(6);
   }
-#undef SPARSE_PHASE
+#undef PC_PHASE
   if (A.prof && lane == 0)
-    for (int i = 0; i < 8; ++i) A.prof[(int64_t)g * 8 + i] = ph[i];
+    for (int i = 0; i < 4; ++i) A.prof[(int64_t)g * 8 + warp * 4 + i] = ph[i];
 }
 
 static unsigned long long* g_sparse_prof = nullptr;
 
+// one resident wave of workers (a worker owns whole partitions; more
+// workers than fit would only queue)
 static int sparse_workers(int32_t n_parts) {
-  int dev = 0, sms = 148;
-  if (cudaGetDevice(&dev) == cudaSuccess)
+  int dev = 0, sms = 148, per_sm = 4;
+  if (cudaGetDevice(&dev) == cudaSuccess) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return std::max(1, std::min((int)n_parts, sms * 16));
+    if (cudaFuncSetAttribute(k_sparse_epoch, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(PcSmem)) == cudaSuccess)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sparse_epoch, 64, sizeof(PcSmem));
+  }
+  return std::max(1, std::min((int)n_parts, sms * std::max(per_sm, 1)));
 }
 
 }  // namespace syscd
@@ -429,11 +599,10 @@ extern "C" int syscd_sparse_epoch(const syscd_sparse_epoch_args* e, void* stream
   A.prof = g_sparse_prof;
   cudaStream_t s = (cudaStream_t)stream;
   SYSCD_CUDA_TRY(cudaMemsetAsync(e->delta_v, 0, e->d * sizeof(float), s));
-  const size_t smem = sizeof(SparseWarpSmem) * kSparseWarps;
+  const size_t smem = sizeof(PcSmem);
   SYSCD_CUDA_TRY(
       cudaFuncSetAttribute(k_sparse_epoch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int blocks = (W + kSparseWarps - 1) / kSparseWarps;
-  k_sparse_epoch<<<blocks, 32 * kSparseWarps, smem, s>>>(A, W);
+  k_sparse_epoch<<<W, 64, smem, s>>>(A, W);
   SYSCD_CUDA_TRY(cudaGetLastError());
   return SYSCD_OK;
 }

@@ -13,11 +13,11 @@ B1="python bench.py --config 1 --steps 2 --warmup 2 --no-e2e --no-cpu --no-ttt"
 $B1 > gpurun_out/plain1.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:k_small_epoch -s 2 -c 1 -o gpurun_out/${R}_cfg1_small $B1 > /dev/null 2>&1
 echo cfg1=$?
-B3="python bench.py --config 3 --scale 0.3 --steps 1 --warmup 2 --no-e2e --no-cpu --no-ttt"
+B3="python bench.py --config 3 --steps 1 --warmup 2 --no-e2e --no-cpu --no-ttt"
 $B3 > gpurun_out/plain3.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:k_grid_epoch -s 2 -c 1 -o gpurun_out/${R}_cfg3s_grid $B3 > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_grid_epoch -s 2 -c 1 -o gpurun_out/${R}_cfg3_grid $B3 > /dev/null 2>&1
 echo cfg3=$?
-B4="python bench.py --config 4 --scale 0.1 --steps 1 --warmup 1 --no-e2e --no-cpu --no-ttt"
+B4="python bench.py --config 4 --steps 1 --warmup 1 --no-e2e --no-cpu --no-ttt"
 $B4 > gpurun_out/plain4.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:k_sparse_epoch -s 1 -c 1 -o gpurun_out/${R}_cfg4s_sparse $B4 > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_sparse_epoch -s 1 -c 1 -o gpurun_out/${R}_cfg4_sparse $B4 > /dev/null 2>&1
 echo cfg4=$?

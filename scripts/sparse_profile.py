@@ -10,7 +10,8 @@ from paper_1911_07722_b200.objective import GlmProblem, SmoothLoss
 scale = float(os.environ.get("SCALE", "1.0"))
 P = int(os.environ.get("P", "512"))
 pb = device_problem(4, scale, 0)
-names = ["form", "copy", "insert", "gather", "chain", "writeback", "zeroing", "longcol"]
+names = ["C.wait_full", "C.chain", "C.wait_next", "C.patch", "P.wait_empty", "P.writeback",
+         "P.produce", "-"]
 L = lib()
 L.syscd_debug_set_sparse_profile.argtypes = [ctypes.c_void_p]
 for name, prob in (("logistic", pb), ("hinge", GlmProblem.build(pb.data, SmoothLoss.hinge(), 1e-6))):
