@@ -197,6 +197,35 @@ __device__ __forceinline__ float coord_step_f(int kind, float lin, float a, floa
   }
 }
 
+// The same steps with the column's reciprocal precomputed off the chain
+// (step_inv): bitwise equal to coord_step_f.  inv < 0 marks aq <= 0 for the
+// Lasso / SVM rows.
+__device__ __forceinline__ float step_inv(int kind, float a, float q, float lam) {
+  const float aq = a * q;
+  if (kind == SYSCD_RIDGE || kind == SYSCD_LOGISTIC) return __frcp_rn(aq + lam);
+  return aq > 0.f ? __frcp_rn(aq) : -1.f;
+}
+
+__device__ __forceinline__ float coord_step_fr(int kind, float lin, float inv, float lam,
+                                               float alpha, float inv_n) {
+  switch (kind) {
+    case SYSCD_RIDGE:
+    case SYSCD_LOGISTIC:
+      return alpha - (lin + lam * alpha) * inv;
+    case SYSCD_LASSO: {
+      if (inv < 0.f) return 0.f;
+      const float z = fmaf(-lin, inv, alpha);
+      const float m = fmaf(-lam, inv, fabsf(z));
+      return m > 0.f ? copysignf(m, z) : 0.f;
+    }
+    default: {  // SVM dual
+      if (inv < 0.f) return 1.f;
+      const float z = fmaf(-(lin - inv_n), inv, alpha);
+      return fminf(fmaxf(z, 0.f), 1.f);
+    }
+  }
+}
+
 // fire-and-forget fp32 add; no "memory" clobber so independent loads (e.g.
 // read-only u in the partition flush) may be scheduled across it
 __device__ __forceinline__ void red_add_f32(float* p, float v) {

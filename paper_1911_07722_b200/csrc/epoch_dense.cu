@@ -221,7 +221,9 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
         for (int c = 0; c < NCH; ++c) {
           mbar_wait(&empty[stage], phase ^ 1u);
           if (c == 0)
-            meta[s & (kMetaRing - 1)] = make_int4(j, __float_as_int(aj), __float_as_int(qj), 0);
+            meta[s & (kMetaRing - 1)] =
+                make_int4(j, __float_as_int(aj), __float_as_int(qj),
+                          __float_as_int(step_inv(args.kind, args.a, qj, args.lam_f)));
           const uint32_t bytes = chunk_bytes[c];
           if (bytes) {
             mbar_arrive_expect_tx(&full[stage], bytes);
@@ -318,7 +320,7 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
         an = (float)coord_step(args.kind, (double)lin, args.a_d, (double)qj, args.lam, (double)aj,
                                args.n_coords);
       } else {
-        an = coord_step_f(args.kind, lin, a, qj, args.lam_f, aj, args.inv_n_f);
+        an = coord_step_fr(args.kind, lin, __int_as_float(mt.w), args.lam_f, aj, args.inv_n_f);
       }
       float delta;
       if (isfinite(an)) {

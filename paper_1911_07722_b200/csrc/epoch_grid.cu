@@ -188,7 +188,8 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
         const float aj = A.alpha[j];
         const float qj = __ldg(A.sq + j);
         mbar_wait(&empty[stage], phase ^ 1u);
-        meta[rel & (kGMeta - 1)] = make_int4(j, __float_as_int(aj), __float_as_int(qj), 0);
+        meta[rel & (kGMeta - 1)] = make_int4(j, __float_as_int(aj), __float_as_int(qj),
+                                             __float_as_int(step_inv(A.kind, A.a, qj, A.lam_f)));
         if (bytes) {
           mbar_arrive_expect_tx(&full[stage], bytes);
           tma_load_1d(ring + (size_t)stage * CTA_ROWS, A.A + (int64_t)j * A.lda + row0, bytes,
@@ -373,7 +374,8 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
                     an = (float)coord_step(A.kind, (double)lin, A.a_d, (double)qj, A.lam,
                                            (double)aj, A.n_coords);
                   } else {
-                    an = coord_step_f(A.kind, lin, a, qj, A.lam_f, aj, A.inv_n_f);
+                    an = coord_step_fr(A.kind, lin, __int_as_float(mt.w), A.lam_f, aj,
+                                       A.inv_n_f);
                   }
                   if (isfinite(an)) {
                     dcur[b] = an - aj;
