@@ -62,12 +62,20 @@ def _dims(cfg_id, scale):
 
 
 def default_solver(cfg_id, n_gpus=1, epochs=None):
+    """BASELINE.json's partitioning at one GPU.  On N GPUs the node groups
+    become the GPUs (K = N) and the partitions per GPU shrink so
+    that K*P -- and with it the surrogate scale a = gamma K P and the
+    per-epoch convergence -- stays that of one GPU: a fixed problem split N
+    ways (strong scaling)."""
     if cfg_id == 0:
-        return SolverConfig(K=1, P=4, bucket_size=16, T1=epochs or 20, seed=0)
+        return SolverConfig(K=n_gpus, P=max(1, 4 // n_gpus), bucket_size=16, T1=epochs or 20,
+                            seed=0)
     if cfg_id == 1:
-        return SolverConfig(K=1, P=64, bucket_size=32, T1=epochs or 30, seed=0)
+        return SolverConfig(K=n_gpus, P=max(1, 64 // n_gpus), bucket_size=32, T1=epochs or 30,
+                            seed=0)
     if cfg_id == 2:
-        return SolverConfig(K=1, P=148, bucket_size=8, T1=epochs or 50, seed=0)
+        return SolverConfig(K=n_gpus, P=max(1, 148 // n_gpus), bucket_size=8, T1=epochs or 50,
+                            seed=0)
     if cfg_id == 3:
         return SolverConfig(K=n_gpus, P=1, bucket_size=8, T1=epochs or 40, seed=0)
     return SolverConfig(K=n_gpus, P=max(8, 512 // n_gpus), bucket_size=64, T1=epochs or 20,
