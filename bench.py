@@ -132,6 +132,7 @@ def f_star_for(problem, cfg_id, epochs=200):
     solved with K=P=1 (exact updates, a = gamma) until the relative model
     change stalls; returns (F*, gap at F*)."""
     from paper_1911_07722_b200 import SolverConfig, compute_reference_optimum, run_syscd
+    from paper_1911_07722_b200.device import Dist
     from paper_1911_07722_b200.objective import RIDGE
     if problem.kind == RIDGE:  # conjugate gradients on the normal equations (cli.py:85-101)
         a_star, f_star = compute_reference_optimum(problem)
@@ -139,7 +140,7 @@ def f_star_for(problem, cfg_id, epochs=200):
     B = 8
     cfg = SolverConfig(K=1, P=1, bucket_size=B, T1=None, max_epochs=epochs, tolerance=1e-7,
                        metrics_every=10_000, compute_gap=True, seed=1)
-    res = run_syscd(problem, cfg)
+    res = run_syscd(problem, cfg, dist=Dist.single())  # the full problem on this rank
     last = res.metrics[-1]
     return last.objective, last.gap
 
@@ -252,8 +253,8 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clk,
     }
-    if not args.no_ttt and rank == 0 and world == 1:
-        out["time_to_target"] = time_to_target(wl, args)
+    if not args.no_ttt:  # every rank takes part (the solve all-reduces dv)
+        out["time_to_target"] = time_to_target(wl, args, dist if world > 1 else None)
     if not args.no_e2e:
         out["e2e"] = e2e_run(args, wl, world, dist)
     if not args.no_cpu and rank == 0 and world == 1:
@@ -276,7 +277,7 @@ def _epoch_kernel_name(dp, eng):
     return "k_dense_epoch"
 
 
-def time_to_target(wl, args, target=1e-4, max_epochs=2000):
+def time_to_target(wl, args, dist=None, target=1e-4, max_epochs=2000):
     """Epochs and summed epoch seconds until the target accuracy.
 
     Primal (ridge / lasso): relative suboptimality (F - F*)/(F0 - F*) with F*
@@ -293,7 +294,7 @@ def time_to_target(wl, args, target=1e-4, max_epochs=2000):
         cap = {1: 300, 4: 60}.get(wl.cfg_id, 200)
         cfg = dataclasses.replace(wl.solver, T1=cap, metrics_every=max(1, cap // 30),
                                   compute_gap=True)
-        res = run_syscd(pb, cfg)
+        res = run_syscd(pb, cfg, dist=dist)
         t, hit, best, secs = 0.0, None, None, []
         for m in res.metrics[1:]:
             secs.append(m.seconds)
@@ -317,7 +318,7 @@ def time_to_target(wl, args, target=1e-4, max_epochs=2000):
     f_star, gap_star = f_star_for(pb, wl.cfg_id)
     cfg = dataclasses.replace(wl.solver, T1=max_epochs if wl.cfg_id != 3 else 200,
                               metrics_every=1, compute_gap=False)
-    res = run_syscd(pb, cfg, f_star=f_star)
+    res = run_syscd(pb, cfg, f_star=f_star, dist=dist)
     f0 = res.metrics[0].objective
     t = 0.0
     hit = None

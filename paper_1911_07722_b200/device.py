@@ -135,6 +135,13 @@ class Dist:
         self.world = tdist.get_world_size() if self.on else 1
         self.group = group
 
+    @classmethod
+    def single(cls):
+        """This process alone (no collectives), also inside a distributed job."""
+        obj = cls.__new__(cls)
+        obj.on, obj.rank, obj.world, obj.group = False, 0, 1, None
+        return obj
+
     def allreduce_(self, t, op="sum"):
         if self.world > 1:
             import torch.distributed as tdist
@@ -153,7 +160,8 @@ class DeviceProblem:
     def __init__(self, problem, store_cols=None, dist=None):
         torch = _torch()
         self.problem = problem
-        self.dist = dist or Dist()
+        # a full (unsharded) problem has nothing to reduce across ranks
+        self.dist = dist if (dist is not None and store_cols is not None) else Dist.single()
         m = problem.data.matrix
         self.kind = problem.kind
         self.d = m.n_rows

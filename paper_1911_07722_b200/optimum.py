@@ -13,7 +13,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .device import DeviceProblem, _matvec_raw, _rmatvec_raw, _torch
+from .device import DeviceProblem, Dist, _matvec_raw, _rmatvec_raw, _torch
 from .objective import RIDGE
 
 
@@ -61,5 +61,5 @@ def compute_reference_optimum(problem, mode="closed-form", max_epochs=2000):
     from .solvers import SolverConfig, run_syscd
     cfg = SolverConfig(algorithm="syscd", K=1, P=1, bucket_size=8, seed=problem.n_coordinates,
                        max_epochs=max_epochs, tolerance=1e-9, metrics_every=10 ** 9)
-    res = run_syscd(problem, cfg)
+    res = run_syscd(problem, cfg, dist=Dist.single())  # the full problem, this process
     return res.alpha, res.metrics[-1].objective

@@ -488,7 +488,7 @@ def run_wild_parallel_scd(problem, cfg, f_star=None):
         raise ValueError("wild solver uses a flat thread pool (K must be 1)")
     torch = _torch()
     if problem._device is None:
-        problem._device = DeviceProblem(problem, dist=Dist())
+        problem._device = DeviceProblem(problem, dist=Dist.single())
     dp = problem._device
     n, d = dp.n_global, dp.d
     f32 = torch.float32
