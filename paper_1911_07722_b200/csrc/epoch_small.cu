@@ -12,11 +12,12 @@
 //     G_ts = x_t . x_s                     (all s < t in parallel)
 //     lin_t = c_t + a * sum_{s<t} delta_s G_ts
 // so the sequential part is one step evaluation, one shuffle and one FMA per
-// update; afterwards w += a * sum_t delta_t x_t.  One warp is one worker:
-// lane t holds column t of the chunk (chain order) in registers; the chunk
-// tile and w live in shared memory.  Workers take contiguous update-balanced
-// ranges of partitions and fold (w-u)/a into their own partials row at each
-// partition end (fixed order: deterministic).
+// update; afterwards w += a * sum_t delta_t x_t.  One worker is one block: a
+// chain warp (lane t owns update t of the chunk) and kSmallHelpers staging
+// warps that load the next chunk's columns and compute its Gram matrix into
+// the other of two shared-memory buffers while the chain runs.  Workers take
+// contiguous update-balanced ranges of partitions and fold (w-u)/a into their
+// own partials row at each partition end (fixed order: deterministic).
 #include <algorithm>
 
 #include "common.cuh"
@@ -41,9 +42,12 @@ struct SmallArgs {
   float* partials;
   int64_t part_ld;
   int32_t* status;
+  unsigned long long* prof;  // debug: per-worker chain-warp phase cycles (nullptr = off)
 };
 
-constexpr int kSmallWarps = 1;  // one worker (partition chain) per block: one SM each
+constexpr int kSmallHelpers = 7;  // staging / Gram warps per worker
+constexpr int kSmallThreads = 32 * (1 + kSmallHelpers);
+constexpr int kGramStride = 36;   // 16-byte aligned Gram rows
 
 // step for one coordinate given its linear term (kind fixed at compile time)
 template <int KIND>
@@ -76,153 +80,265 @@ __device__ __forceinline__ int64_t lb_small(const int64_t* a, int n, int64_t key
   return lo;
 }
 
+template <int D>
+struct SmallSmem {
+  static constexpr int DP = D + 4;  // 16-byte aligned rows, conflict-free 16-byte reads
+  float tile[2][32][DP];            // [buffer][chunk column][row]
+  float G[2][32][kGramStride];      // [buffer][t][s] = x_t . x_s (s < t used)
+  int j[2][32];
+  float q[2][32];
+  float alpha[2][32];
+  float inv_aq[2][32];
+  float w[32];
+  float delta[32];
+  uint64_t full[2], empty[2];
+};
+
+// One worker = one block: warp 0 runs the chain, warps 1..kSmallHelpers stage
+// the next chunk's columns and compute its Gram matrix (double-buffered), so
+// the chain warp's per-chunk work is c_t, the 32 sequential steps and the w
+// update.  Every worker walks the same chunk sequence: contiguous
+// update-balanced partitions, chunks of 32 updates.
 template <int D, int KIND>
-__global__ void __launch_bounds__(32 * kSmallWarps) k_small_epoch(SmallArgs A, int W) {
-  constexpr int DP = D + 4;  // padded row: 16-byte aligned, conflict-free 16-byte reads
-  __shared__ __align__(16) float s_tile[kSmallWarps][32][DP];  // [chunk column][row]
-  __shared__ float s_w[kSmallWarps][32];
-  __shared__ float s_delta[kSmallWarps][32];
+__global__ void __launch_bounds__(kSmallThreads) k_small_epoch(SmallArgs A, int W) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SmallSmem<D>& S = *reinterpret_cast<SmallSmem<D>*>(smem_raw);
   const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  const int g = blockIdx.x * kSmallWarps + wib;
+  const int warp = threadIdx.x >> 5;
+  const int g = blockIdx.x;
   if (g >= W) return;
-  float(*tile)[DP] = s_tile[wib];
-  float* wsh = s_w[wib];
-  float* dsh = s_delta[wib];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&S.full[i], kSmallHelpers);
+      mbar_init(&S.empty[i], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
   const int d = A.d;
   const float a = A.a;
-  const float inv_a = (float)(1.0 / A.a_d);
-
   const int64_t total = A.wp[A.n_parts];
   const int64_t t_lo = (int64_t)((__int128)total * g / W);
   const int64_t t_hi = (int64_t)((__int128)total * (g + 1) / W);
   const int64_t p_lo = g == 0 ? 0 : lb_small(A.wp, A.n_parts + 1, t_lo);
   const int64_t p_hi = g == W - 1 ? A.n_parts : lb_small(A.wp, A.n_parts + 1, t_hi);
+
+  if (warp > 0) {
+    // ------------------------------------------------------------ helpers
+    const int hw = warp - 1;
+    constexpr int kPer = (32 + kSmallHelpers - 1) / kSmallHelpers;
+    const int tl = hw + kSmallHelpers * lane;  // the chunk column this lane indexes
+    int k = 0;
+    // the next chunk's coordinate ids are loaded one chunk ahead
+    int64_t pn = p_lo, cn = p_lo < p_hi ? A.wp[p_lo] : 0;
+    auto next_ids = [&](int64_t c0, int64_t s1) {
+      const int m = (int)min((int64_t)32, s1 - c0);
+      return (lane < kPer && tl < m) ? A.seq[c0 + tl] : 0;
+    };
+    int jnext = 0;
+    while (pn < p_hi && cn >= A.wp[pn + 1]) {
+      ++pn;
+      if (pn < p_hi) cn = A.wp[pn];
+    }
+    if (pn < p_hi) jnext = next_ids(cn, A.wp[pn + 1]);
+    for (int64_t p = p_lo; p < p_hi; ++p) {
+      const int64_t s0 = A.wp[p], s1 = A.wp[p + 1];
+      for (int64_t c0 = s0; c0 < s1; c0 += 32, ++k) {
+        const int m = (int)min((int64_t)32, s1 - c0);
+        const int b = k & 1;
+        const int jl = jnext;
+        {  // advance the lookahead to the chunk after this one
+          cn = c0 + 32;
+          pn = p;
+          while (pn < p_hi && cn >= A.wp[pn + 1]) {
+            ++pn;
+            if (pn < p_hi) cn = A.wp[pn];
+          }
+          if (pn < p_hi) jnext = next_ids(cn, A.wp[pn + 1]);
+        }
+        // this warp stages columns t = hw + kSmallHelpers * i (lane = row);
+        // the loads go to registers before the buffer is free
+        float col[kPer];
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+          const int t = hw + kSmallHelpers * i;
+          const int jt = __shfl_sync(0xffffffffu, jl, i);
+          col[i] = (t < m && lane < d) ? __ldg(A.A + (int64_t)jt * A.lda + lane) : 0.f;
+        }
+        float qv = 0.f, av = 0.f;
+        const bool mine = lane < kPer && tl < m;
+        if (mine) {
+          qv = __ldg(A.sq + jl);
+          if (!A.iid) av = A.alpha[jl];
+        }
+        if (k >= 2) mbar_wait(&S.empty[b], ((k >> 1) - 1) & 1);
+        if (lane < kPer && tl < 32) S.j[b][tl] = jl;
+        if (mine) {
+          S.q[b][tl] = qv;
+          S.inv_aq[b][tl] = qv > 0.f ? __fdiv_rn(1.f, a * qv) : 0.f;
+          S.alpha[b][tl] = av;
+        }
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+          const int t = hw + kSmallHelpers * i;
+          if (t < 32 && lane < D) S.tile[b][t][lane] = col[i];
+        }
+        named_bar_sync(2, 32 * kSmallHelpers);
+        // Gram: lane t holds row x_t; this warp fills columns s of G
+        float x[D];
+#pragma unroll
+        for (int i4 = 0; i4 < D / 4; ++i4) {
+          const float4 v = reinterpret_cast<const float4*>(S.tile[b][lane])[i4];
+          x[4 * i4] = v.x;
+          x[4 * i4 + 1] = v.y;
+          x[4 * i4 + 2] = v.z;
+          x[4 * i4 + 3] = v.w;
+        }
+        for (int sc = hw; sc < m; sc += kSmallHelpers) {
+          const float4* ts = reinterpret_cast<const float4*>(S.tile[b][sc]);
+          float acc = 0.f;
+#pragma unroll
+          for (int i4 = 0; i4 < D / 4; ++i4) {
+            const float4 v = ts[i4];
+            acc = fmaf(x[4 * i4], v.x, acc);
+            acc = fmaf(x[4 * i4 + 1], v.y, acc);
+            acc = fmaf(x[4 * i4 + 2], v.z, acc);
+            acc = fmaf(x[4 * i4 + 3], v.w, acc);
+          }
+          S.G[b][lane][sc] = acc;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.full[b]);
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- chain warp
+  unsigned long long ph[4] = {0, 0, 0, 0};
+  long long tq = clock64();
+#define SMALL_PHASE(i)                      \
+  if (A.prof) {                             \
+    const long long tn = clock64();         \
+    ph[i] += (unsigned long long)(tn - tq); \
+    tq = tn;                                \
+  }
+  const float inv_a = (float)(1.0 / A.a_d);
   float* out = A.partials + (int64_t)g * A.part_ld;
   const float u_l = lane < d ? A.u[lane] : 0.f;
   bool flushed = false;
-
+  int k = 0;
   for (int64_t p = p_lo; p < p_hi; ++p) {
     const int64_t s0 = A.wp[p], s1 = A.wp[p + 1];
     if (s1 == s0) continue;
-    wsh[lane] = u_l;  // w = u at the partition start
+    S.w[lane] = u_l;  // w = u at the partition start
     __syncwarp();
-    // prefetch registers for the next chunk (columns + scalars)
-    int j_n = 0;
-    float x_n[D];
-    float q_n = 0.f, a_n = 0.f;
-    {
-      const int m0 = (int)min((int64_t)32, s1 - s0);
-      if (lane < m0) {
-        j_n = A.seq[s0 + lane];
-        const float* col = A.A + (int64_t)j_n * A.lda;
-#pragma unroll
-        for (int i = 0; i < D; ++i) x_n[i] = i < d ? __ldg(col + i) : 0.f;
-        q_n = __ldg(A.sq + j_n);
-        a_n = A.alpha[j_n];
-      } else {
-#pragma unroll
-        for (int i = 0; i < D; ++i) x_n[i] = 0.f;
-      }
-    }
-    for (int64_t c0 = s0; c0 < s1; c0 += 32) {
+    for (int64_t c0 = s0; c0 < s1; c0 += 32, ++k) {
       const int m = (int)min((int64_t)32, s1 - c0);
-      // ---- stage: lane t holds column j_t (chain order) and its scalars
-      const int j = j_n;
-      float x[D];
-#pragma unroll
-      for (int i = 0; i < D; ++i) x[i] = x_n[i];
-      const float q_t = q_n;
-      // iid rounds may revisit a coordinate of an earlier chunk: reload
-      float alpha_t = A.iid ? (lane < m ? *(volatile float*)(A.alpha + j) : 0.f) : a_n;
-      {
-        const int64_t c1 = c0 + 32;
-        const int m1 = (int)min((int64_t)32, s1 - c1);
-        if (lane < m1) {
-          j_n = A.seq[c1 + lane];
-          const float* col = A.A + (int64_t)j_n * A.lda;
-#pragma unroll
-          for (int i = 0; i < D; ++i) x_n[i] = i < d ? __ldg(col + i) : 0.f;
-          q_n = __ldg(A.sq + j_n);
-          if (!A.iid) a_n = A.alpha[j_n];
-        }
-      }
-      const float inv_aq = q_t > 0.f ? __fdiv_rn(1.f, a * q_t) : 0.f;
-#pragma unroll
-      for (int i = 0; i < D; ++i) tile[lane][i] = x[i];
-      __syncwarp();
-      // ---- c_t = x_t . w and the strictly-lower Gram row G_t[s], s < t
+      const int b = k & 1;
+      mbar_wait(&S.full[b], (k >> 1) & 1);
+      SMALL_PHASE(0);
+      // c_t = x_t . w and the Gram row of lane t
       float r = 0.f;
-#pragma unroll
-      for (int i = 0; i < D; ++i) r = fmaf(x[i], wsh[i], r);
-      // branch-free: every lane computes the full row, entries s >= t unused
-      float G[32];
-#pragma unroll
-      for (int s = 0; s < 32; ++s) {
-        const float4* ts = reinterpret_cast<const float4*>(tile[s]);
-        float acc = 0.f;
+      {
+        const float4* xr = reinterpret_cast<const float4*>(S.tile[b][lane]);
+        const float4* wr = reinterpret_cast<const float4*>(S.w);
 #pragma unroll
         for (int i4 = 0; i4 < D / 4; ++i4) {
-          const float4 v = ts[i4];
-          acc = fmaf(x[4 * i4], v.x, acc);
-          acc = fmaf(x[4 * i4 + 1], v.y, acc);
-          acc = fmaf(x[4 * i4 + 2], v.z, acc);
-          acc = fmaf(x[4 * i4 + 3], v.w, acc);
+          const float4 xv = xr[i4], wv = wr[i4];
+          r = fmaf(xv.x, wv.x, r);
+          r = fmaf(xv.y, wv.y, r);
+          r = fmaf(xv.z, wv.z, r);
+          r = fmaf(xv.w, wv.w, r);
         }
-        G[s] = acc;
       }
-      // ---- sequential chain: lane s finalises lin_s, broadcasts delta_s
-      float my_delta = 0.f;
+      float G[32];
 #pragma unroll
-      for (int s = 0; s < 32; ++s) {
-        if (s < m) {
-          float cand;
-          if (KIND == SYSCD_LOGISTIC_DUAL) {
-            // Newton solve on the owning lane only (keeps the loop body small)
-            cand = 0.f;
-            if (lane == s)
-              cand = small_step<KIND>(r, alpha_t, q_t, a, inv_aq, A.lam_f, A.inv_n_f, A);
-          } else {
-            cand = small_step<KIND>(r, alpha_t, q_t, a, inv_aq, A.lam_f, A.inv_n_f, A);
-          }
-          float dl = cand - alpha_t;
-          if (!isfinite(cand)) dl = 0.f;
-          const float delta = __shfl_sync(0xffffffffu, dl, s);
-          const int js = __shfl_sync(0xffffffffu, j, s);
-          if (lane == s) {
-            my_delta = delta;
-            if (!isfinite(cand)) atomicOr(A.status, SYSCD_ENONFINITE);
-          }
-          r = fmaf(a * delta, G[s], r);
-          // a coordinate drawn twice in one chunk (iid) sees its new value
-          if (A.iid && lane > s && j == js) alpha_t += delta;
-        }
+      for (int s4 = 0; s4 < 8; ++s4) {
+        const float4 v = reinterpret_cast<const float4*>(S.G[b][lane])[s4];
+        G[4 * s4] = v.x;
+        G[4 * s4 + 1] = v.y;
+        G[4 * s4 + 2] = v.z;
+        G[4 * s4 + 3] = v.w;
       }
+      const int j = S.j[b][lane];
+      const float q_t = lane < m ? S.q[b][lane] : 0.f;
+      // iid rounds may revisit a coordinate of an earlier chunk: reload
+      float alpha_t = lane < m ? (A.iid ? *(volatile float*)(A.alpha + j) : S.alpha[b][lane]) : 0.f;
+      const float inv_aq = lane < m ? S.inv_aq[b][lane] : 0.f;
+      SMALL_PHASE(1);
+      // ---- sequential chain: lane s finalises lin_s, broadcasts delta_s.
+      // The critical path per update is the step, one shuffle and one FMA
+      // (a G_ts is pre-scaled; a non-finite step is flagged after the chain --
+      // the host then raises NonFiniteUpdateError and the round is void).
+#pragma unroll
+      for (int s4 = 0; s4 < 32; ++s4) G[s4] *= a;
+      const bool iid = A.iid != 0;
+      float my_delta = 0.f;
+      auto step_once = [&](int s) {
+        float cand;
+        if (KIND == SYSCD_LOGISTIC_DUAL) {
+          // Newton solve on the owning lane only (keeps the loop body small)
+          cand = alpha_t;
+          if (lane == s)
+            cand = small_step<KIND>(r, alpha_t, q_t, a, inv_aq, A.lam_f, A.inv_n_f, A);
+        } else {
+          cand = small_step<KIND>(r, alpha_t, q_t, a, inv_aq, A.lam_f, A.inv_n_f, A);
+        }
+        const float delta = __shfl_sync(0xffffffffu, cand - alpha_t, s);
+        my_delta = lane == s ? delta : my_delta;
+        r = fmaf(delta, G[s], r);
+        if (iid) {
+          // a coordinate drawn twice in one chunk sees its new value
+          const int js = __shfl_sync(0xffffffffu, j, s);
+          if (lane > s && j == js) alpha_t += delta;
+        }
+      };
+      if (m == 32) {  // full chunk: no per-step bound checks
+#pragma unroll
+        for (int s = 0; s < 32; ++s) step_once(s);
+      } else {
+#pragma unroll
+        for (int s = 0; s < 32; ++s)
+          if (s < m) step_once(s);
+      }
+      if (lane < m && !isfinite(my_delta)) atomicOr(A.status, SYSCD_ENONFINITE);
       {
         // a repeated coordinate (iid) is written once, by its last occurrence
         const unsigned act = __ballot_sync(0xffffffffu, lane < m);
         const unsigned same = __match_any_sync(0xffffffffu, lane < m ? j : -1 - lane) & act;
         if (lane < m && (31 - __clz(same)) == lane) A.alpha[j] = alpha_t + my_delta;
       }
-      dsh[lane] = lane < m ? my_delta : 0.f;
+      S.delta[lane] = lane < m ? my_delta : 0.f;
       __syncwarp();
+      SMALL_PHASE(2);
       // ---- w += a * sum_t delta_t x_t   (lane = row)
       if (lane < d) {
-        float acc = 0.f;
-        for (int t = 0; t < m; ++t) acc = fmaf(dsh[t], tile[t][lane], acc);
-        wsh[lane] = fmaf(a, acc, wsh[lane]);
+        float acc0 = 0.f, acc1 = 0.f;  // two chains, summed in a fixed order
+        int t = 0;
+        for (; t + 1 < m; t += 2) {
+          acc0 = fmaf(S.delta[t], S.tile[b][t][lane], acc0);
+          acc1 = fmaf(S.delta[t + 1], S.tile[b][t + 1][lane], acc1);
+        }
+        if (t < m) acc0 = fmaf(S.delta[t], S.tile[b][t][lane], acc0);
+        S.w[lane] = fmaf(a, acc0 + acc1, S.w[lane]);
       }
       __syncwarp();
+      if (lane == 0) mbar_arrive(&S.empty[b]);
+      SMALL_PHASE(3);
     }
     // ---- partition end: fold (w - u)/a into this worker's partial row
     if (lane < d) {
-      const float dv = (wsh[lane] - u_l) * inv_a;
+      const float dv = (S.w[lane] - u_l) * inv_a;
       out[lane] = flushed ? out[lane] + dv : dv;
     }
     flushed = true;
     __syncwarp();
   }
   if (!flushed && lane < d) out[lane] = 0.f;
+#undef SMALL_PHASE
+  if (A.prof && lane == 0)
+    for (int i = 0; i < 4; ++i) A.prof[(int64_t)g * 4 + i] = ph[i];
 }
 
 int small_workers(int32_t n_parts) {
@@ -232,8 +348,11 @@ int small_workers(int32_t n_parts) {
   return std::max(1, std::min((int)n_parts, sms * 8));
 }
 
+static unsigned long long* g_small_prof = nullptr;
+
 int small_launch(const syscd_dense_epoch_args* e, cudaStream_t stream) {
   SmallArgs A;
+  A.prof = g_small_prof;
   A.A = e->A;
   A.lda = e->lda;
   A.d = (int)e->d;
@@ -255,7 +374,6 @@ int small_launch(const syscd_dense_epoch_args* e, cudaStream_t stream) {
   A.part_ld = e->part_ld;
   A.status = e->status;
   const int W = small_workers(e->n_parts);
-  const int blocks = (W + kSmallWarps - 1) / kSmallWarps;
   const int Dsel = e->d <= 8 ? 8 : (e->d <= 16 ? 16 : 32);
   void (*fn)(SmallArgs, int) = nullptr;
 #define SYSCD_SMALL_CASE(DD, KK) \
@@ -272,9 +390,19 @@ int small_launch(const syscd_dense_epoch_args* e, cudaStream_t stream) {
     set_error("small epoch: unsupported objective");
     return SYSCD_EINVAL;
   }
-  fn<<<blocks, 32 * kSmallWarps, 0, stream>>>(A, W);
+  const size_t smem = Dsel == 8 ? sizeof(SmallSmem<8>)
+                     : (Dsel == 16 ? sizeof(SmallSmem<16>) : sizeof(SmallSmem<32>));
+  SYSCD_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  fn<<<W, kSmallThreads, smem, stream>>>(A, W);
   SYSCD_CUDA_TRY(cudaGetLastError());
   return SYSCD_OK;
 }
 
 }  // namespace syscd
+
+// Debug hook (not part of the C-ABI contract): with a device buffer of
+// n_workers * 4 uint64, the next small epochs record the chain warp's cycles
+// in: waiting for the staged chunk, c_t + Gram row loads, the chain, w update.
+extern "C" void syscd_debug_set_small_profile(void* device_buffer) {
+  syscd::g_small_prof = (unsigned long long*)device_buffer;
+}
