@@ -608,19 +608,38 @@ def _run(problem, cfg, f_star, dist):
     total = 0
     start = torch.cuda.Event(enable_timing=True)
     stop = torch.cuda.Event(enable_timing=True)
+    # With a fixed round count, rounds without a metrics row are queued back
+    # to back: no host synchronisation, the update counts stay on the device
+    # and prev tracks the previous round's alpha with a device copy.  A
+    # non-finite step or alpha is then detected at the next metrics row.
+    lazy = cfg.T1 is not None and not cfg.verify and not cfg.record_alpha
+    pending = 0  # rounds whose update counts have not been read yet
     for t1 in range(cfg.n_rounds):
+        last = t1 == cfg.n_rounds - 1
+        row_due = (t1 + 1) % cfg.metrics_every == 0 or last
         start.record()
         eng.global_round(t1)
         stop.record()
+        if lazy and not row_due:
+            prev.copy_(eng.alpha)
+            pending += 1
+            continue
         stop.synchronize()
         elapsed = start.elapsed_time(stop) / 1e3
         eng.check_status()
         upd = 0
         for t2 in range(cfg.T2):
             upd += eng.updates_last_round(t1 * cfg.T2 + t2)
-        upd_t = torch.tensor([upd], dtype=torch.int64, device="cuda")
-        upd = int(dist.allreduce_(upd_t).item())
-        total += upd
+        if pending:
+            lo = (t1 - pending) * cfg.T2
+            total_prev = int(eng.upd_dev[lo:t1 * cfg.T2].sum().item())
+        else:
+            total_prev = 0
+        pending = 0
+        cnt = torch.tensor([upd, total_prev], dtype=torch.int64, device="cuda")
+        dist.allreduce_(cnt)
+        upd, total_prev = int(cnt[0].item()), int(cnt[1].item())
+        total += upd + total_prev
         if cfg.verify:
             for t2 in range(cfg.T2):
                 if cfg.sampling == "perm" and not eng.census_ok(t1 * cfg.T2 + t2):
@@ -641,9 +660,8 @@ def _run(problem, cfg, f_star, dist):
         dist.allreduce_(m_abs, op="max")
         rel = float(d_rel) / max(1.0, float(m_abs))
         prev.copy_(eng.alpha)
-        last = t1 == cfg.n_rounds - 1
         stop_now = cfg.T1 is None and rel < cfg.tolerance
-        if (t1 + 1) % cfg.metrics_every == 0 or last or stop_now:
+        if row_due or stop_now:
             metrics.append(metrics_row(t1 + 1, elapsed, upd, rel))
         if cfg.record_alpha:
             snaps.append(eng.alpha_global())

@@ -209,3 +209,22 @@ def test_dual_alpha_stays_in_box(cuda):
         res = run_syscd(pb, SolverConfig(K=1, P=4, bucket_size=8, T1=6, compute_gap=True))
         assert np.all(res.alpha >= 0) and np.all(res.alpha <= 1)
         assert all(m.gap >= -1e-6 for m in res.metrics)
+
+
+def test_sparse_metrics_rows_and_lazy_rounds(cuda):
+    """metrics_every=k: rows at k, 2k, ... and the last round; the rounds in
+    between run without host synchronisation but leave the same state, update
+    totals and per-row rel_change (vs the previous round) as k=1."""
+    from paper_1911_07722_b200 import SolverConfig, run_syscd
+    pb, _ = both(0, 0.05)
+    kw = dict(K=1, P=4, bucket_size=4, T1=12, seed=5)
+    full = run_syscd(pb, SolverConfig(**kw))
+    lazy = run_syscd(pb, SolverConfig(metrics_every=5, **kw))
+    assert [m.epoch for m in lazy.metrics] == [0, 5, 10, 12]
+    assert lazy.total_updates == full.total_updates
+    assert np.array_equal(lazy.alpha, full.alpha)
+    by_epoch = {m.epoch: m for m in full.metrics}
+    for m in lazy.metrics[1:]:
+        ref = by_epoch[m.epoch]
+        assert m.objective == ref.objective and m.updates == ref.updates
+        assert m.rel_change == ref.rel_change
