@@ -133,6 +133,54 @@ __global__ void k_dense_sqnorm(int64_t d, int64_t n, int64_t lda, const float* _
   }
 }
 
+// Tall columns (d >= kColBlockMinD): one 256-thread block per column, 16-byte
+// loads, four fp64 accumulators per thread and a fixed-order block reduction
+// (deterministic).  Optional w (nullptr: squared norm).
+constexpr int kColBlockThreads = 256;
+constexpr int64_t kColBlockMinD = 4096;
+
+__global__ void __launch_bounds__(kColBlockThreads)
+    k_dense_coldot_block(int64_t d, int64_t n, int64_t lda, const float* __restrict__ A,
+                         const double* __restrict__ w, double* __restrict__ out_d,
+                         float* __restrict__ out_f) {
+  __shared__ double red[kColBlockThreads / 32];
+  const int tid = threadIdx.x;
+  for (int64_t j = blockIdx.x; j < n; j += gridDim.x) {
+    const float* col = A + j * lda;  // lda % 4 == 0, 16-byte aligned columns
+    const int64_t d4 = d >> 2;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    const float4* c4 = reinterpret_cast<const float4*>(col);
+    for (int64_t q = tid; q < d4; q += kColBlockThreads) {
+      const float4 x = __ldg(c4 + q);
+      if (w) {
+        const double2 w0 = __ldg(reinterpret_cast<const double2*>(w) + 2 * q);
+        const double2 w1 = __ldg(reinterpret_cast<const double2*>(w) + 2 * q + 1);
+        a0 = fma((double)x.x, w0.x, a0);
+        a1 = fma((double)x.y, w0.y, a1);
+        a2 = fma((double)x.z, w1.x, a2);
+        a3 = fma((double)x.w, w1.y, a3);
+      } else {
+        a0 = fma((double)x.x, (double)x.x, a0);
+        a1 = fma((double)x.y, (double)x.y, a1);
+        a2 = fma((double)x.z, (double)x.z, a2);
+        a3 = fma((double)x.w, (double)x.w, a3);
+      }
+    }
+    for (int64_t i = 4 * d4 + tid; i < d; i += kColBlockThreads)
+      a0 = fma((double)col[i], w ? w[i] : (double)col[i], a0);
+    double acc = warp_sum_d((a0 + a1) + (a2 + a3));
+    if ((tid & 31) == 0) red[tid >> 5] = acc;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int k = 0; k < kColBlockThreads / 32; ++k) t += red[k];
+      if (out_d) out_d[j] = t;
+      if (out_f) out_f[j] = (float)t;
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void k_sparse_matvec(int64_t n, const int64_t* __restrict__ cp, const int32_t* __restrict__ ri,
                                 const float* __restrict__ vals, const float* __restrict__ x,
                                 double* __restrict__ out) {
@@ -389,7 +437,11 @@ extern "C" int syscd_dense_rmatvec(int64_t d, int64_t n, int64_t lda, const floa
     set_error("syscd_dense_rmatvec: invalid arguments");
     return SYSCD_EINVAL;
   }
-  k_dense_rmatvec<<<grid_for(n * 32, 256), 256, 0, (cudaStream_t)stream>>>(d, n, lda, A, w, out);
+  if (d >= kColBlockMinD && ((uintptr_t)w & 15) == 0 && (lda % 4) == 0)
+    k_dense_coldot_block<<<(int)(n < 148 * 16 ? n : 148 * 16), kColBlockThreads, 0,
+                           (cudaStream_t)stream>>>(d, n, lda, A, w, out, nullptr);
+  else
+    k_dense_rmatvec<<<grid_for(n * 32, 256), 256, 0, (cudaStream_t)stream>>>(d, n, lda, A, w, out);
   SYSCD_CUDA_TRY(cudaGetLastError());
   return SYSCD_OK;
 }
@@ -400,7 +452,11 @@ extern "C" int syscd_dense_col_sq_norms(int64_t d, int64_t n, int64_t lda, const
     set_error("syscd_dense_col_sq_norms: invalid arguments");
     return SYSCD_EINVAL;
   }
-  k_dense_sqnorm<<<grid_for(n * 32, 256), 256, 0, (cudaStream_t)stream>>>(d, n, lda, A, out);
+  if (d >= kColBlockMinD && (lda % 4) == 0)
+    k_dense_coldot_block<<<(int)(n < 148 * 16 ? n : 148 * 16), kColBlockThreads, 0,
+                           (cudaStream_t)stream>>>(d, n, lda, A, nullptr, nullptr, out);
+  else
+    k_dense_sqnorm<<<grid_for(n * 32, 256), 256, 0, (cudaStream_t)stream>>>(d, n, lda, A, out);
   SYSCD_CUDA_TRY(cudaGetLastError());
   return SYSCD_OK;
 }
