@@ -146,7 +146,6 @@ def f_star_for(problem, cfg_id, epochs=200):
 
 
 def run_ours(args):
-    import numpy as np
     import torch
     from paper_1911_07722_b200 import run_syscd
     from paper_1911_07722_b200.configs import workload
@@ -342,7 +341,6 @@ def time_to_target(wl, args, dist=None, target=1e-4, max_epochs=2000):
 def e2e_run(args, wl, world, dist):
     """Public API on host data: pinned upload + run_syscd + alpha download."""
     import dataclasses
-    import numpy as np
     import torch
     from paper_1911_07722_b200 import (ColumnMatrix, GlmProblem, LabeledDataset,
                                        run_syscd)
@@ -388,7 +386,6 @@ def e2e_run(args, wl, world, dist):
 
 def cpu_baseline(wl, eng, args):
     from oracle import cpu_baseline as cb
-    from oracle import objectives as ob
     pb = wl.problem
     kind = ["ridge", "logistic", "lasso", "svm_dual", "logistic_dual"][pb.kind]
     m = pb.data.matrix

@@ -30,7 +30,7 @@ from .dataset import (
     LabeledDataset,
     padded_ld,
 )
-from .objective import GlmProblem, Regularizer, SmoothLoss
+from .objective import GlmProblem, SmoothLoss
 from .solvers import SolverConfig
 
 # lambda = LASSO_RATIO * ||A^T y||_inf for config 2 (calibrated so that about

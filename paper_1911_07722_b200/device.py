@@ -15,9 +15,9 @@ import ctypes
 
 import numpy as np
 
-from ._lib import call, lib
+from ._lib import call
 from .dataset import padded_ld
-from .objective import LASSO, LOGISTIC, LOGISTIC_DUAL, RIDGE, SVM_DUAL
+from .objective import LASSO, LOGISTIC, RIDGE, SVM_DUAL
 
 
 def _torch():
