@@ -80,3 +80,30 @@ def test_libsvm_file_through_the_solver(cuda, tmp_path):
     o2 = np.array([m.objective for m in r2.metrics])
     assert np.max(np.abs(o1 - o2) / np.abs(o1)) < 1e-6
     assert np.linalg.norm(r1.alpha - r2.alpha) / np.linalg.norm(r1.alpha) < 1e-5
+
+
+def test_libsvm_examples_orientation_dual(cuda, tmp_path):
+    """A LIBSVM file in the example orientation drives the SVM dual: same
+    trajectory as the dataset it was written from, alpha in its box."""
+    import numpy as np
+    from paper_1911_07722_b200 import (COORDINATES_ARE_EXAMPLES, GlmProblem, LabeledDataset,
+                                       SmoothLoss, SolverConfig, generate_synthetic_sparse,
+                                       run_syscd)
+    from paper_1911_07722_b200.dataset import ColumnMatrix, load_libsvm, save_libsvm
+    ds = generate_synthetic_sparse(300, 24, 0.3, 3)
+    path = str(tmp_path / "d.svm")
+    save_libsvm(ds, path)
+    ex = load_libsvm(path, n_features=24, orientation=COORDINATES_ARE_EXAMPLES)
+    assert (ex.matrix.n_rows, ex.matrix.n_cols) == (24, 300)
+    # the same data built in memory: columns = examples
+    dense_t = ds.matrix.to_dense().T.copy()
+    mem = LabeledDataset(ColumnMatrix(24, 300, dense=dense_t), ds.labels,
+                         COORDINATES_ARE_EXAMPLES)
+    cfg = SolverConfig(K=1, P=4, bucket_size=8, seed=1, T1=4, compute_gap=True)
+    r1 = run_syscd(GlmProblem.build(ex, SmoothLoss.hinge(), 1.0 / 300), cfg)
+    r2 = run_syscd(GlmProblem.build(mem, SmoothLoss.hinge(), 1.0 / 300), cfg)
+    o1 = np.array([m.objective for m in r1.metrics])
+    o2 = np.array([m.objective for m in r2.metrics])
+    assert np.max(np.abs(o1 - o2) / np.maximum(np.abs(o2), 1e-12)) < 1e-5
+    assert np.all(r1.alpha >= 0) and np.all(r1.alpha <= 1)
+    assert all(m.gap >= -1e-9 for m in r1.metrics)
