@@ -276,6 +276,34 @@ def _epoch_kernel_name(dp, eng):
     return "k_dense_epoch"
 
 
+def dual_suboptimality(pb, res, k, target, epochs=150):
+    """(D - D*)/(D0 - D*) along a dual run, with D* from a K=P=1 solve (exact
+    coordinate updates) certified by its duality gap; reported
+    only when the certificate is tighter than the target."""
+    from paper_1911_07722_b200 import SolverConfig, run_syscd
+    from paper_1911_07722_b200.device import Dist
+    cfg = SolverConfig(K=1, P=1, bucket_size=8, T1=None, max_epochs=epochs, tolerance=1e-8,
+                       metrics_every=10_000, compute_gap=True, seed=1)
+    ref = run_syscd(pb, cfg, dist=Dist.single())
+    d_star, gap_star = ref.metrics[-1].objective, ref.metrics[-1].gap
+    d0 = res.metrics[0].objective
+    scale = max(d0 - d_star, 1e-300)
+    out = {"definition": "(D-D*)/(D0-D*), D* by a K=P=1 GPU solve certified by its gap",
+           "d_star": d_star, "d_star_gap": gap_star, "certified": gap_star <= 0.1 * target * scale,
+           "solve_epochs": ref.metrics[-1].epoch}
+    if not out["certified"]:
+        return out
+    t, hit, best = 0.0, None, None
+    for m in res.metrics[1:]:
+        t += m.seconds * k
+        rel = (m.objective - d_star) / scale
+        best = rel if best is None else min(best, rel)
+        if hit is None and rel <= target:
+            hit = {"epoch": m.epoch, "seconds": t}
+    out.update(hit=hit, best_rel_subopt=best)
+    return out
+
+
 def time_to_target(wl, args, dist=None, target=1e-4, max_epochs=2000):
     """Epochs and summed epoch seconds until the target accuracy.
 
@@ -307,13 +335,16 @@ def time_to_target(wl, args, dist=None, target=1e-4, max_epochs=2000):
             best = rel if best is None else min(best, rel)
             if hit is None and rel <= target:
                 hit = {"epoch": m.epoch, "seconds": t}
-        return {"target": target, "definition": "duality gap / |P(w)| (dual objective)",
-                "hit": hit, "best_rel_gap": best, "epochs_run": res.metrics[-1].epoch,
-                "epoch_seconds_total_est": t,
-                "rel_gap_at_config_epochs": next((m.gap / max(abs(m.gap - m.objective), 1e-300)
-                                                  for m in res.metrics
-                                                  if m.epoch >= wl.solver.T1), None),
-                "config_epochs": wl.solver.T1}
+        out = {"target": target, "definition": "duality gap / |P(w)| (dual objective)",
+               "hit": hit, "best_rel_gap": best, "epochs_run": res.metrics[-1].epoch,
+               "epoch_seconds_total_est": t,
+               "rel_gap_at_config_epochs": next((m.gap / max(abs(m.gap - m.objective), 1e-300)
+                                                 for m in res.metrics
+                                                 if m.epoch >= wl.solver.T1), None),
+               "config_epochs": wl.solver.T1}
+        if pb.n_coordinates <= 4_000_000:
+            out["suboptimality"] = dual_suboptimality(pb, res, k, target)
+        return out
     f_star, gap_star = f_star_for(pb, wl.cfg_id)
     cfg = dataclasses.replace(wl.solver, T1=max_epochs if wl.cfg_id != 3 else 200,
                               metrics_every=1, compute_gap=False)

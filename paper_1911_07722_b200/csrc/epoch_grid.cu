@@ -176,17 +176,22 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
     const uint32_t bytes = (uint32_t)(((valid + 3) / 4) * 16);
     const uint64_t policy = A.evict_first ? policy_evict_first() : policy_evict_last();
     uint32_t stage = 0, phase = 0;
+    // coordinate ids, alpha and q of 32 columns at a time (lane-parallel), so
+    // no dependent global load sits between two TMA issues
     int jreg = 0;
+    float areg = 0.f, qreg = 0.f;
     for (int64_t s = s_begin; s < s_end; ++s) {
       const int64_t rel = s - s_begin;
       if ((rel & 31) == 0) {
         const int64_t q = s + lane;
         jreg = q < s_end ? A.seq[q] : 0;
+        areg = q < s_end ? A.alpha[jreg] : 0.f;
+        qreg = q < s_end ? __ldg(A.sq + jreg) : 0.f;
       }
       const int j = __shfl_sync(0xffffffffu, jreg, (int)(rel & 31));
+      const float aj = __shfl_sync(0xffffffffu, areg, (int)(rel & 31));
+      const float qj = __shfl_sync(0xffffffffu, qreg, (int)(rel & 31));
       if (lane == 0) {
-        const float aj = A.alpha[j];
-        const float qj = __ldg(A.sq + j);
         mbar_wait(&empty[stage], phase ^ 1u);
         meta[rel & (kGMeta - 1)] = make_int4(j, __float_as_int(aj), __float_as_int(qj),
                                              __float_as_int(step_inv(A.kind, A.a, qj, A.lam_f)));
