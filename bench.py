@@ -244,7 +244,9 @@ def run_ours(args):
             "peak_source": peak_kind,
             "unit": "GB/s",
             "frac": achieved / hbm,
-            "traffic": None,
+            "traffic": (ncu_traffic(args.config, world) or {}).get("bytes"),
+            "traffic_unit": "bytes per launch (dram read + write, ncu --set full)",
+            "traffic_source": (ncu_traffic(args.config, world) or {}).get("source"),
             "kernel_ms": k_avg,
             "kernel_share_of_step": k_avg / ms_per_step,
             "algorithmic_bytes_per_launch": local_a_bytes,
@@ -262,6 +264,31 @@ def run_ours(args):
         print(json.dumps(out), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def ncu_traffic(cfg_id, world):
+    """DRAM bytes (read + write) per launch of the epoch kernel from the
+    committed `ncu --set full` capture of this configuration (profiles/),
+    or None when there is none (or the run is sharded differently)."""
+    import glob
+    import re
+    if world != 1:
+        return None
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_cfg{cfg_id}_*_ncu_summary.txt")))
+    if not files:
+        return None
+    unit = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    total = 0.0
+    found = 0
+    with open(files[-1]) as f:
+        for line in f:
+            m = re.match(r"dram__bytes_(read|write)\.sum\s+([0-9.]+)\s+(\w+)", line)
+            if m:
+                total += float(m.group(2)) * unit.get(m.group(3), float("nan"))
+                found += 1
+    if found != 2:
+        return None
+    return {"bytes": total, "gb": total / 1e9, "source": os.path.relpath(files[-1], ROOT)}
 
 
 def _epoch_kernel_name(dp, eng):
