@@ -228,3 +228,118 @@ def test_sparse_metrics_rows_and_lazy_rounds(cuda):
         ref = by_epoch[m.epoch]
         assert m.objective == ref.objective and m.updates == ref.updates
         assert m.rel_change == ref.rel_change
+
+
+def _edge_pair(kind, d, n, seed, zero_cols=(), lam=None):
+    """The same tiny problem for the GPU mirror and the oracle (dense store)."""
+    from paper_1911_07722_b200 import (COORDINATES_ARE_EXAMPLES, COORDINATES_ARE_FEATURES,
+                                       ColumnMatrix, GlmProblem, LabeledDataset, SmoothLoss)
+    g = np.random.default_rng(seed)
+    A = g.standard_normal((d, n)).astype(np.float32)
+    for j in zero_cols:
+        A[:, j] = 0.0
+    if kind in ("ridge", "lasso"):
+        y = g.standard_normal(d)
+        lam = lam or (0.5 if kind == "ridge" else 0.05 * float(np.abs(A.T @ y).max()))
+        ds = LabeledDataset(ColumnMatrix(d, n, dense=A), y, COORDINATES_ARE_FEATURES)
+        pb = GlmProblem.build(ds, SmoothLoss.squared_error(), lam,
+                              reg="l1" if kind == "lasso" else "l2")
+        ob = O.OracleProblem(O.OracleMatrix(dense=A.astype(np.float64)), y, kind, lam)
+    else:
+        y = np.where(g.random(n) < 0.5, -1.0, 1.0)
+        lam = lam or 1.0 / n
+        ds = LabeledDataset(ColumnMatrix(d, n, dense=A), y, COORDINATES_ARE_EXAMPLES)
+        loss = SmoothLoss.hinge() if kind == "svm_dual" else SmoothLoss.logistic()
+        pb = GlmProblem.build(ds, loss, lam)
+        ob = O.OracleProblem(O.OracleMatrix(dense=A.astype(np.float64) * y[None, :]),
+                             np.zeros(d), kind, lam)
+    return pb, ob
+
+
+@pytest.mark.parametrize("kind", ["ridge", "lasso", "svm_dual", "logistic_dual"])
+@pytest.mark.parametrize("d,n,kw", [
+    (1, 1, dict(K=1, P=1, bucket_size=8)),          # one coordinate, one row
+    (5, 3, dict(K=1, P=1, bucket_size=8)),          # n < B: a single partial bucket
+    (31, 40, dict(K=2, P=2, bucket_size=4)),        # small-d kernel, K > 1 on one GPU
+    (33, 40, dict(K=1, P=4, bucket_size=4)),        # just above the small-d threshold
+    (600, 50, dict(K=1, P=5, bucket_size=3, sampling="iid", T3=2, T4=4)),
+])
+def test_edge_geometries(cuda, kind, d, n, kw):
+    from paper_1911_07722_b200 import SolverConfig, run_syscd
+    pb, ob = _edge_pair(kind, d, n, seed=d * 131 + n, zero_cols=(0,) if n > 2 else ())
+    res = run_syscd(pb, SolverConfig(seed=3, T1=4, compute_gap=True, **kw))
+    ores = O.run_syscd(ob, O.OracleConfig(seed=3, T1=4, with_gap=True, **kw))
+    assert_parity(res, ores)
+    if kind in ("svm_dual", "logistic_dual"):
+        assert np.all(res.alpha >= 0) and np.all(res.alpha <= 1)
+    if n > 2 and kind in ("ridge", "lasso"):
+        assert res.alpha[0] == 0.0  # an all-zero column never moves
+
+
+def _sparse_edge_pair(kind, d, n, seed):
+    """CSC problem with empty columns, ordinary columns and columns longer than
+    the sparse kernel's chunk (> 512 nonzeros: the streamed long-column path)."""
+    from paper_1911_07722_b200 import (COORDINATES_ARE_EXAMPLES, COORDINATES_ARE_FEATURES,
+                                       ColumnMatrix, GlmProblem, LabeledDataset, SmoothLoss)
+    g = np.random.default_rng(seed)
+    ptr, idx, val = [0], [], []
+    for j in range(n):
+        k = 0 if j % 7 == 3 else (int(g.integers(520, min(d, 1500))) if j % 5 == 1
+                                  else int(g.integers(1, 40)))
+        rows = np.sort(g.choice(d, size=k, replace=False))
+        idx.extend(rows.tolist())
+        val.extend(g.standard_normal(k).astype(np.float32).tolist())
+        ptr.append(len(idx))
+    ptr = np.array(ptr, dtype=np.int64)
+    idx = np.array(idx, dtype=np.int64)
+    val = np.array(val, dtype=np.float32)
+    m = ColumnMatrix(d, n, csc=(ptr, idx, val))
+    if kind in ("ridge", "lasso"):
+        y = g.standard_normal(d)
+        lam = 0.5 if kind == "ridge" else 0.3
+        ds = LabeledDataset(m, y, COORDINATES_ARE_FEATURES)
+        pb = GlmProblem.build(ds, SmoothLoss.squared_error(), lam,
+                              reg="l1" if kind == "lasso" else "l2")
+        ob = O.OracleProblem(O.OracleMatrix(csc=(ptr, idx, val.astype(np.float64)), shape=(d, n)),
+                             y, kind, lam)
+    else:
+        y = np.where(g.random(n) < 0.5, -1.0, 1.0)
+        lam = 1.0 / n
+        ds = LabeledDataset(m, y, COORDINATES_ARE_EXAMPLES)
+        loss = SmoothLoss.hinge() if kind == "svm_dual" else SmoothLoss.logistic()
+        pb = GlmProblem.build(ds, loss, lam)
+        vals = val.astype(np.float64) * np.repeat(y, np.diff(ptr))
+        ob = O.OracleProblem(O.OracleMatrix(csc=(ptr, idx, vals), shape=(d, n)), np.zeros(d),
+                             kind, lam)
+    return pb, ob
+
+
+@pytest.mark.parametrize("kind", ["ridge", "lasso", "svm_dual", "logistic_dual"])
+@pytest.mark.parametrize("kw", [dict(K=1, P=3, bucket_size=4),
+                                dict(K=2, P=2, bucket_size=2, sampling="iid", T4=3)])
+def test_sparse_edge_columns(cuda, kind, kw):
+    from paper_1911_07722_b200 import SolverConfig, run_syscd
+    pb, ob = _sparse_edge_pair(kind, 2000, 60, seed=11)
+    res = run_syscd(pb, SolverConfig(seed=4, T1=4, compute_gap=True, **kw))
+    ores = O.run_syscd(ob, O.OracleConfig(seed=4, T1=4, with_gap=True, **kw))
+    assert_parity(res, ores)
+
+
+def test_sparse_exact_logistic_single_worker(cuda):
+    """K=P=1 primal logistic on a CSC store (exact Newton on the live v, incl.
+    empty and long columns) against the oracle's _logistic_newton path."""
+    from paper_1911_07722_b200 import (COORDINATES_ARE_FEATURES, ColumnMatrix, GlmProblem,
+                                       LabeledDataset, SmoothLoss, SolverConfig, run_syscd)
+    pb_r, _ = _sparse_edge_pair("ridge", 2000, 40, seed=5)
+    ptr, idx, val = pb_r.data.matrix.csc()
+    g = np.random.default_rng(9)
+    y = np.where(g.random(2000) < 0.4, -1.0, 1.0)
+    m = ColumnMatrix(2000, 40, csc=(ptr, idx.astype(np.int64), val))
+    pb = GlmProblem.build(LabeledDataset(m, y, COORDINATES_ARE_FEATURES), SmoothLoss.logistic(),
+                          0.7)
+    ob = O.OracleProblem(O.OracleMatrix(csc=(ptr, idx.astype(np.int64), val.astype(np.float64)),
+                                        shape=(2000, 40)), y, "logistic", 0.7)
+    kw = dict(K=1, P=1, bucket_size=4)
+    res = run_syscd(pb, SolverConfig(seed=2, T1=3, **kw))
+    ores = O.run_syscd(ob, O.OracleConfig(seed=2, T1=3, **kw))
+    assert_parity(res, ores)
