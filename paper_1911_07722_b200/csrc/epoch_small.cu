@@ -90,7 +90,7 @@ struct SmallSmem {
   float alpha[2][32];
   float inv_aq[2][32];
   float w[32];
-  float delta[32];
+  alignas(16) float delta[32];
   uint64_t full[2], empty[2];
 };
 
@@ -128,61 +128,72 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_epoch(SmallArgs A, int 
     const int hw = warp - 1;
     constexpr int kPer = (32 + kSmallHelpers - 1) / kSmallHelpers;
     const int tl = hw + kSmallHelpers * lane;  // the chunk column this lane indexes
-    int k = 0;
-    // the next chunk's coordinate ids are loaded one chunk ahead
-    int64_t pn = p_lo, cn = p_lo < p_hi ? A.wp[p_lo] : 0;
-    auto next_ids = [&](int64_t c0, int64_t s1) {
-      const int m = (int)min((int64_t)32, s1 - c0);
-      return (lane < kPer && tl < m) ? A.seq[c0 + tl] : 0;
+    // Chunks are staged two ahead of their use: the registers hold the
+    // columns (and q, alpha) of the next two chunks, so the global loads of
+    // a chunk are in flight for about two chunk times before its buffer is
+    // free.  A chunk cursor walks the partitions' chunks in order.
+    struct Cursor {
+      int64_t p, c0;
     };
-    int jnext = 0;
-    while (pn < p_hi && cn >= A.wp[pn + 1]) {
-      ++pn;
-      if (pn < p_hi) cn = A.wp[pn];
-    }
-    if (pn < p_hi) jnext = next_ids(cn, A.wp[pn + 1]);
-    for (int64_t p = p_lo; p < p_hi; ++p) {
-      const int64_t s0 = A.wp[p], s1 = A.wp[p + 1];
-      for (int64_t c0 = s0; c0 < s1; c0 += 32, ++k) {
-        const int m = (int)min((int64_t)32, s1 - c0);
-        const int b = k & 1;
-        const int jl = jnext;
-        {  // advance the lookahead to the chunk after this one
-          cn = c0 + 32;
-          pn = p;
-          while (pn < p_hi && cn >= A.wp[pn + 1]) {
-            ++pn;
-            if (pn < p_hi) cn = A.wp[pn];
-          }
-          if (pn < p_hi) jnext = next_ids(cn, A.wp[pn + 1]);
-        }
-        // this warp stages columns t = hw + kSmallHelpers * i (lane = row);
-        // the loads go to registers before the buffer is free
-        float col[kPer];
+    auto valid = [&](const Cursor& c) { return c.p < p_hi; };
+    auto advance = [&](Cursor c) {
+      c.c0 += 32;
+      while (c.p < p_hi && c.c0 >= A.wp[c.p + 1]) {
+        ++c.p;
+        if (c.p < p_hi) c.c0 = A.wp[c.p];
+      }
+      return c;
+    };
+    struct Staged {
+      float col[kPer];
+      float q, alpha;
+      int j, m;
+    };
+    auto load = [&](const Cursor& c, Staged& st) {
+      st.m = 0;
+      st.j = 0;
+      st.q = st.alpha = 0.f;
+      if (valid(c)) st.m = (int)min((int64_t)32, A.wp[c.p + 1] - c.c0);
+      const bool mine = lane < kPer && tl < st.m;
+      if (mine) st.j = A.seq[c.c0 + tl];
 #pragma unroll
-        for (int i = 0; i < kPer; ++i) {
-          const int t = hw + kSmallHelpers * i;
-          const int jt = __shfl_sync(0xffffffffu, jl, i);
-          col[i] = (t < m && lane < d) ? __ldg(A.A + (int64_t)jt * A.lda + lane) : 0.f;
-        }
-        float qv = 0.f, av = 0.f;
-        const bool mine = lane < kPer && tl < m;
-        if (mine) {
-          qv = __ldg(A.sq + jl);
-          if (!A.iid) av = A.alpha[jl];
-        }
-        if (k >= 2) mbar_wait(&S.empty[b], ((k >> 1) - 1) & 1);
-        if (lane < kPer && tl < 32) S.j[b][tl] = jl;
-        if (mine) {
-          S.q[b][tl] = qv;
-          S.inv_aq[b][tl] = qv > 0.f ? __fdiv_rn(1.f, a * qv) : 0.f;
-          S.alpha[b][tl] = av;
-        }
+      for (int i = 0; i < kPer; ++i) {
+        const int t = hw + kSmallHelpers * i;
+        const int jt = __shfl_sync(0xffffffffu, st.j, i);
+        st.col[i] = (t < st.m && lane < d) ? __ldg(A.A + (int64_t)jt * A.lda + lane) : 0.f;
+      }
+      if (mine) {
+        st.q = __ldg(A.sq + st.j);
+        if (!A.iid) st.alpha = A.alpha[st.j];
+      }
+    };
+    Cursor c_cur{p_lo, p_lo < p_hi ? A.wp[p_lo] - 32 : 0};
+    c_cur = advance(c_cur);  // the first non-empty chunk
+    Cursor c_nxt = advance(c_cur);
+    Staged cur, nxt;
+    load(c_cur, cur);
+    load(c_nxt, nxt);
+    for (int k = 0; valid(c_cur); ++k) {
+      const int b = k & 1;
+      const int m = cur.m;
+      if (k >= 2) mbar_wait(&S.empty[b], ((k >> 1) - 1) & 1);
+      if (lane < kPer && tl < 32) S.j[b][tl] = cur.j;
+      if (lane < kPer && tl < m) {
+        S.q[b][tl] = cur.q;
+        S.inv_aq[b][tl] = cur.q > 0.f ? __fdiv_rn(1.f, a * cur.q) : 0.f;
+        S.alpha[b][tl] = cur.alpha;
+      }
 #pragma unroll
-        for (int i = 0; i < kPer; ++i) {
-          const int t = hw + kSmallHelpers * i;
-          if (t < 32 && lane < D) S.tile[b][t][lane] = col[i];
-        }
+      for (int i = 0; i < kPer; ++i) {
+        const int t = hw + kSmallHelpers * i;
+        if (t < 32 && lane < D) S.tile[b][t][lane] = cur.col[i];
+      }
+      // shift the staging window and put the chunk after next in flight
+      cur = nxt;
+      c_cur = c_nxt;
+      c_nxt = advance(c_nxt);
+      load(c_nxt, nxt);
+      {
         named_bar_sync(2, 32 * kSmallHelpers);
         // Gram: lane t holds row x_t; this warp fills columns s of G
         float x[D];
@@ -314,14 +325,18 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_epoch(SmallArgs A, int 
       SMALL_PHASE(2);
       // ---- w += a * sum_t delta_t x_t   (lane = row)
       if (lane < d) {
-        float acc0 = 0.f, acc1 = 0.f;  // two chains, summed in a fixed order
-        int t = 0;
-        for (; t + 1 < m; t += 2) {
-          acc0 = fmaf(S.delta[t], S.tile[b][t][lane], acc0);
-          acc1 = fmaf(S.delta[t + 1], S.tile[b][t + 1][lane], acc1);
+        // four chains (deltas of t >= m are zero), summed in a fixed order
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        const float4* dl4 = reinterpret_cast<const float4*>(S.delta);
+#pragma unroll
+        for (int t4 = 0; t4 < 8; ++t4) {
+          const float4 dv4 = dl4[t4];
+          acc[0] = fmaf(dv4.x, S.tile[b][4 * t4][lane], acc[0]);
+          acc[1] = fmaf(dv4.y, S.tile[b][4 * t4 + 1][lane], acc[1]);
+          acc[2] = fmaf(dv4.z, S.tile[b][4 * t4 + 2][lane], acc[2]);
+          acc[3] = fmaf(dv4.w, S.tile[b][4 * t4 + 3][lane], acc[3]);
         }
-        if (t < m) acc0 = fmaf(S.delta[t], S.tile[b][t][lane], acc0);
-        S.w[lane] = fmaf(a, acc0 + acc1, S.w[lane]);
+        S.w[lane] = fmaf(a, (acc[0] + acc[1]) + (acc[2] + acc[3]), S.w[lane]);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.empty[b]);
