@@ -19,8 +19,9 @@
  *    SYSCD_ENONFINITE (-> NonFiniteUpdateError, objective.py:13-14,
  *    solvers.py:307-308), SYSCD_ECUDA (CUDA/NCCL error -> RuntimeError).
  *    syscd_last_error() returns a thread-local message for the last failure.
- *  - No global mutable state besides that message: concurrent calls on
- *    distinct problems are safe.
+ *  - No global mutable state besides that message, per-device caches of the
+ *    kernel-configuration queries (guarded) and the debug hooks (not part of
+ *    this ABI): concurrent calls on distinct problems are safe.
  */
 #ifndef SYSCD_B200_H_
 #define SYSCD_B200_H_
@@ -142,7 +143,8 @@ int syscd_dense_epoch(const syscd_dense_epoch_args* e, void* stream);
 
 
 /* Sparse CSC store (int64 col_ptr, int32 row_idx, fp32 values); sparse
- * col_dot / col_axpy of dataset.py:77-78,90-91.  One warp per worker.  The
+ * col_dot / col_axpy of dataset.py:77-78,90-91.  A worker is one 64-thread
+ * block (a chain warp and a staging warp).  The
  * private replicas live in dv_work (n_workers x d 64-bit words, zero-filled
  * once at allocation): each word is (tag << 32 | fp32 bits) and reads as 0
  * unless its tag is the running partition's, so replicas never need
