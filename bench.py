@@ -404,13 +404,19 @@ def e2e_run(args, wl, world, dist):
                                        run_syscd)
     pb = wl.problem
     m = pb.data.matrix
-    if m.storage_kind != "dense":
-        return None
-    At_dev = m._dev_dense if m._dev_dense is not None else None
-    if At_dev is None:
-        return None
-    host = torch.empty(At_dev.shape, dtype=torch.float32, pin_memory=True)
-    host.copy_(At_dev)
+    if m.storage_kind == "dense":
+        if m._dev_dense is None:
+            return None
+        hosts = [torch.empty(m._dev_dense.shape, dtype=torch.float32, pin_memory=True)]
+        hosts[0].copy_(m._dev_dense)
+    else:
+        if m._dev_csc is None:
+            return None
+        hosts = []
+        for t in m._dev_csc:
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t)
+            hosts.append(h)
     labels = pb.data.labels.copy()
     cfg = dataclasses.replace(wl.solver, metrics_every=10_000_000)
     steps = 2
@@ -420,8 +426,9 @@ def e2e_run(args, wl, world, dist):
         if world > 1:
             torch.distributed.barrier()
         t0 = time.perf_counter()
-        dev = host.to("cuda", non_blocking=True)
-        mm = ColumnMatrix.from_device(dev, m.n_rows)
+        devs = [h.to("cuda", non_blocking=True) for h in hosts]
+        mm = (ColumnMatrix.from_device(devs[0], m.n_rows) if m.storage_kind == "dense" else
+              ColumnMatrix.from_device_csc(*devs, m.n_rows))
         ds = LabeledDataset(mm, labels, pb.data.orientation)
         p2 = GlmProblem.build(ds, pb.loss, pb.reg.lam, reg=pb.reg.kind)
         res = run_syscd(p2, cfg)
@@ -431,11 +438,12 @@ def e2e_run(args, wl, world, dist):
         if s > 0:
             times.append(dt)
             upd += res.total_updates
-        del dev, mm, ds, p2
+        del devs, mm, ds, p2
     tt = torch.tensor([max(times) * len(times)], dtype=torch.float64, device="cuda")
     dist.allreduce_(tt, op="max")
     return {"value": upd / float(tt), "unit": "updates/s",
-            "h2d_bytes_per_step": int(host.numel() * 4 + labels.size * 8),
+            "h2d_bytes_per_step": int(sum(h.numel() * h.element_size() for h in hosts)
+                                      + labels.size * 8),
             "d2h_bytes_per_step": int(m.n_cols * 8),
             "step": f"GlmProblem.build + run_syscd over {cfg.T1} epochs on a host-resident "
                     "problem (pinned H2D of A and y, column norms, fresh device state, alpha D2H)",
