@@ -65,11 +65,8 @@ struct DenseArgs {
 
 constexpr int kMetaRing = 64;
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
+// debug timeline stamp: the SM cycle counter (CTA 0 only, so one clock)
+__device__ __forceinline__ unsigned long long gtimer() { return (unsigned long long)clock64(); }
 constexpr int kMaxCluster = 16;
 
 template <int NTC, int RC, int NCH>
@@ -127,7 +124,11 @@ __device__ __forceinline__ int64_t lower_bound_i64(const int64_t* a, int n, int6
   return lo;
 }
 
-template <class Cfg>
+// KIND: the step is compiled in (SYSCD_RIDGE also serves the primal-logistic
+// surrogate, which has the same closed form); the hot loop carries only its
+// own step -- the logistic-dual fp64 Newton would otherwise sit in every
+// instance's loop.
+template <class Cfg, int KIND>
 __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args) {
   constexpr int NTC = Cfg::kNTC;
   constexpr int NWC = Cfg::kNWC;
@@ -316,11 +317,11 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
       }
       if (args.iid) aj = *(volatile float*)(args.alpha + j);
       float an;
-      if (args.kind == SYSCD_LOGISTIC_DUAL) {
+      if (KIND == SYSCD_LOGISTIC_DUAL) {
         an = (float)coord_step(args.kind, (double)lin, args.a_d, (double)qj, args.lam, (double)aj,
                                args.n_coords);
       } else {
-        an = coord_step_fr(args.kind, lin, __int_as_float(mt.w), args.lam_f, aj, args.inv_n_f);
+        an = coord_step_fr(KIND, lin, __int_as_float(mt.w), args.lam_f, aj, args.inv_n_f);
       }
       float delta;
       if (isfinite(an)) {
@@ -403,7 +404,7 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
 // ---------------------------------------------------------------------------
 struct KernelEntry {
   int ntc, rc, nch;
-  const void* fn;
+  const void* fn[4];  // per step kind: ridge (and primal logistic), lasso, svm dual, logistic dual
   int threads;
   int max_clusters[kMaxCluster + 1];  // per cluster size, 0 = unknown, -1 = not launchable
 };
@@ -414,7 +415,10 @@ static KernelEntry make_entry() {
   e.ntc = NTC;
   e.rc = RC;
   e.nch = NCH;
-  e.fn = (const void*)&k_dense_epoch<DenseCfg<NTC, RC, NCH>>;
+  e.fn[0] = (const void*)&k_dense_epoch<DenseCfg<NTC, RC, NCH>, SYSCD_RIDGE>;
+  e.fn[1] = (const void*)&k_dense_epoch<DenseCfg<NTC, RC, NCH>, SYSCD_LASSO>;
+  e.fn[2] = (const void*)&k_dense_epoch<DenseCfg<NTC, RC, NCH>, SYSCD_SVM_DUAL>;
+  e.fn[3] = (const void*)&k_dense_epoch<DenseCfg<NTC, RC, NCH>, SYSCD_LOGISTIC_DUAL>;
   e.threads = NTC + 32;
   for (int i = 0; i <= kMaxCluster; ++i) e.max_clusters[i] = 0;
   return e;
@@ -443,8 +447,10 @@ static int choose_stages(const KernelEntry& e, size_t smem_budget) {
 
 static int query_max_clusters(KernelEntry& e, int C, int stages, size_t smem) {
   if (e.max_clusters[C] != 0) return e.max_clusters[C];
-  cudaFuncSetAttribute(e.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (C > 8) cudaFuncSetAttribute(e.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  for (const void* fn : e.fn) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (C > 8) cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(C, 1, 1);
   cfg.blockDim = dim3(e.threads, 1, 1);
@@ -457,7 +463,7 @@ static int query_max_clusters(KernelEntry& e, int C, int stages, size_t smem) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
-  cudaError_t err = cudaOccupancyMaxActiveClusters(&n, e.fn, &cfg);
+  cudaError_t err = cudaOccupancyMaxActiveClusters(&n, e.fn[0], &cfg);
   if (getenv("SYSCD_DEBUG"))
     fprintf(stderr, "[syscd] cfg (%d,%d,%d) C=%d smem=%zu -> clusters=%d (%s)\n", e.ntc, e.rc,
             e.nch, C, smem, n, cudaGetErrorString(err));
@@ -544,7 +550,7 @@ using namespace syscd;
 
 static void* g_dbg_buffer = nullptr;
 // Debug hook (not part of the header ABI): when set to a device buffer of
-// >= 512*6 uint64, the next dense epochs record %globaltimer at the step
+// >= 512*6 uint64, the next dense epochs record SM clock cycles at the step
 // phases of CTA 0 (start, dot done, CTA reduce done, exchange done, step
 // done, axpy done).
 extern "C" void syscd_debug_set_timeline(void* device_buffer) { g_dbg_buffer = device_buffer; }
@@ -647,6 +653,9 @@ extern "C" int syscd_dense_epoch(const syscd_dense_epoch_args* e, void* stream) 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   void* params[] = {&args};
-  SYSCD_CUDA_TRY(cudaLaunchKernelExC(&cfg, ke.fn, params));
+  const int slot = e->kind == SYSCD_LASSO ? 1
+                   : e->kind == SYSCD_SVM_DUAL ? 2
+                   : e->kind == SYSCD_LOGISTIC_DUAL ? 3 : 0;
+  SYSCD_CUDA_TRY(cudaLaunchKernelExC(&cfg, ke.fn[slot], params));
   return SYSCD_OK;
 }

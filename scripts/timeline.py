@@ -19,7 +19,7 @@ eng.global_round(3)
 torch.cuda.synchronize()
 L.syscd_debug_set_timeline(None)
 t = buf.view(512, 6).cpu().numpy().astype(np.float64)
-t = t[t[:, 0] > 0]
+t = t[t[:, 0] > 0] / 1.965  # SM cycles -> ns at the 1965 MHz boost clock
 d = np.diff(t, axis=1)
 step = np.diff(t[:, 0])
 names = ["dot(wait+pass)", "cta_reduce+push", "exchange_wait", "step", "axpy(+release)"]
