@@ -44,6 +44,7 @@ constexpr int kGNB = 16;    // global record slots (events), > 2*LL+2
 constexpr int kGMeta = 64;  // metadata ring (columns)
 constexpr int kGTot = 8;    // totals ring in shared memory (events), > LL+1
 constexpr int kGVal = 32;   // max values per event record
+constexpr int kGRecent = 64;  // iid: recently resolved (j, alpha) per math warp, >= prefetch lead
 
 struct GridArgs {
   const float* A;
@@ -60,6 +61,7 @@ struct GridArgs {
   float inv_n_f;
   double a_d, lam, n_coords;
   int32_t kind;
+  int32_t iid;
   int32_t stages;
   int32_t evict_first;
   float* out;                // [d] summed replicas (one worker row)
@@ -75,7 +77,7 @@ __device__ __forceinline__ unsigned long long gtimer_g() {
 }
 
 struct GridSmem {
-  size_t ring, full, empty, totbar, tot, red, meta, total;
+  size_t ring, full, empty, totbar, tot, red, meta, recent, total;
 };
 
 __host__ __device__ inline size_t galign(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -98,6 +100,8 @@ __host__ __device__ inline GridSmem grid_smem(int stages, int cta_rows) {
   o = galign(o, 16);
   L.meta = o;
   o += kGMeta * 16;
+  L.recent = o;
+  o += 16 * kGRecent * 8;  // one ring per math warp (<= 16 warps)
   L.total = galign(o, 128);
   return L;
 }
@@ -146,6 +150,7 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
   float* tot = reinterpret_cast<float*>(smem + Lo.tot);
   float* red = reinterpret_cast<float*>(smem + Lo.red);
   int4* meta = reinterpret_cast<int4*>(smem + Lo.meta);
+  int2* recent = reinterpret_cast<int2*>(smem + Lo.recent);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -158,6 +163,7 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
   const int64_t s_end = A.wp[A.n_parts];
 
   for (int i = tid; i < S * CTA_ROWS; i += blockDim.x) ring[i] = 0.f;
+  for (int i = tid; i < 16 * kGRecent; i += blockDim.x) recent[i] = make_int2(-1, 0);
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
@@ -272,6 +278,11 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
     uint32_t stage = 0, phase = 0;
     bool flushed = false;
     int64_t ebase = 0;  // event (publication) index of the partition's block 0
+    // iid: the prefetched alpha of a coordinate drawn again within the
+    // prefetch window is stale; every math warp keeps the same ring of the
+    // last kGRecent resolved (j, alpha) and takes the newest match
+    int2* rcnt_ring = recent + warp * kGRecent;
+    uint32_t rcnt = 0;
     for (int p = 0; p < A.n_parts; ++p) {
       const int64_t col0 = A.wp[p] - s_begin;  // flattened column index of column 0
       const int m = (int)(A.wp[p + 1] - A.wp[p]);
@@ -372,8 +383,18 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
                   for (int k = 0; k < b; ++k) lin = fmaf(a * dcur[k], t[Lay::gin(b, k)], lin);
                   const int4 mt = meta[(col0 + col) & (kGMeta - 1)];
                   const int j = mt.x;
-                  const float aj = __int_as_float(mt.y);
+                  float aj = __int_as_float(mt.y);
                   const float qj = __int_as_float(mt.z);
+                  if (A.iid) {
+                    const int2 r0 = rcnt_ring[(rcnt - 1 - lane) & (kGRecent - 1)];
+                    const int2 r1 = rcnt_ring[(rcnt - 33 - lane) & (kGRecent - 1)];
+                    const unsigned m0 = __ballot_sync(0xffffffffu, r0.x == j);
+                    const unsigned m1 = __ballot_sync(0xffffffffu, r1.x == j);
+                    if (m0 | m1) {
+                      const int kk = m0 ? __ffs(m0) - 1 : 32 + __ffs(m1) - 1;
+                      aj = __int_as_float(rcnt_ring[(rcnt - 1 - kk) & (kGRecent - 1)].y);
+                    }
+                  }
                   float an;
                   if (A.kind == SYSCD_LOGISTIC_DUAL) {
                     an = (float)coord_step(A.kind, (double)lin, A.a_d, (double)qj, A.lam,
@@ -387,6 +408,13 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
                     if (cta == 0 && tid == 0) A.alpha[j] = an;
                   } else if (cta == 0 && tid == 0) {
                     atomicOr(A.status, SYSCD_ENONFINITE);
+                  }
+                  if (A.iid) {
+                    __syncwarp();
+                    if (lane == 0)
+                      rcnt_ring[rcnt & (kGRecent - 1)] = make_int2(j, __float_as_int(aj + dcur[b]));
+                    __syncwarp();
+                    ++rcnt;
                   }
                 }
               }
@@ -499,10 +527,6 @@ int grid_launch(const syscd_dense_epoch_args* e, void* workspace, int64_t ws_byt
     set_error("syscd_dense_epoch: grid workspace too small");
     return SYSCD_EINVAL;
   }
-  if (e->iid) {
-    set_error("iid sampling is not supported when d needs the grid-wide kernel");
-    return SYSCD_EINVAL;
-  }
   const GridEntry& ge = g_grid_table[idx];
   SYSCD_CUDA_TRY(cudaFuncSetAttribute(ge.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
@@ -516,6 +540,7 @@ int grid_launch(const syscd_dense_epoch_args* e, void* workspace, int64_t ws_byt
   A.seq = e->seq;
   A.wp = e->work_prefix;
   A.n_parts = e->n_parts;
+  A.iid = e->iid;
   A.a = (float)e->a;
   A.lam_f = (float)e->lam;
   A.inv_n_f = (float)(1.0 / e->n_coords);

@@ -50,6 +50,9 @@ CASES = [
     (2, 0.5, dict(K=1, P=1, bucket_size=8, T1=3)),
     (2, 0.5, dict(K=1, P=3, bucket_size=4, T1=2)),
     (4, 0.0002, dict(K=2, P=3, bucket_size=16, sampling="iid", T3=3, T4=4, T1=3)),
+    # iid on the grid-wide kernel: repeats inside the prefetch window
+    (3, 0.15, dict(K=1, P=1, bucket_size=8, sampling="iid", T3=12, T4=8, T1=3)),
+    (2, 0.5, dict(K=1, P=2, bucket_size=4, sampling="iid", T3=20, T4=6, T1=2)),
 ]
 
 
