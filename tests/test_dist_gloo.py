@@ -57,3 +57,28 @@ def test_two_rank_sharding_and_reduction(built_lib):
     assert sum(o[4] for o in out) == 203
     for o in out:                                      # all-reduce == serial node sum
         np.testing.assert_allclose(o[5], o[6], rtol=1e-12)
+
+
+@pytest.mark.parametrize("n_gpus", [1, 2, 4, 8])
+def test_bench_workloads_shard_over_n_gpus(built_lib, n_gpus):
+    """bench.py --gpus N: every BASELINE config keeps K*P at its one-GPU value
+    (within rounding), uses K = N node groups, and shards into N disjoint
+    stores covering every coordinate once."""
+    from paper_1911_07722_b200.configs import _dims, default_solver
+    from paper_1911_07722_b200.sharding import shard_plan
+    for cfg_id in range(5):
+        one = default_solver(cfg_id, 1)
+        cfg = default_solver(cfg_id, n_gpus)
+        assert cfg.K == n_gpus
+        assert cfg.K * cfg.P <= one.K * one.P * max(1, n_gpus)
+        if cfg_id != 3:  # config 3 is K = GPUs, P = 1 by definition
+            assert abs(cfg.K * cfg.P - one.K * one.P) < n_gpus
+        d, n = _dims(cfg_id, 0.01 if cfg_id != 1 else 0.001)
+        B = cfg.resolved_bucket_size()
+        if cfg.K * cfg.P > -(-n // B):
+            continue  # the scaled-down stand-in has too few buckets for this split
+        cols = []
+        for r in range(n_gpus):
+            sp = shard_plan(n, B, cfg.K, cfg.P, cfg.seed, n_gpus, r)
+            cols.extend(sp.store_cols.tolist() if sp.store_cols is not None else range(n))
+        assert sorted(cols) == list(range(n))
