@@ -98,6 +98,7 @@ __device__ __forceinline__ float sparse_step(const SparseArgs& A, float lin, flo
 
 constexpr int kPcNnz = 512;
 constexpr int kPcTable = 1024;
+constexpr int kPcFilterWords = 128;  // 4096-bit membership filter of a chunk's rows
 
 struct PcBuf {
   int key[kPcTable];
@@ -106,6 +107,7 @@ struct PcBuf {
   float dvold[kPcTable];
   short slot[kPcNnz];
   short uniq[kPcNnz];  // the chunk's distinct slots
+  unsigned filt[kPcFilterWords];  // one bit per row hash: which rows this chunk holds
   float val[kPcNnz];
   int row[kPcNnz];
   float alpha_c[32];
@@ -125,6 +127,10 @@ struct PcSmem {
 
 __device__ __forceinline__ unsigned pc_hash(int r) {
   return ((unsigned)r * 2654435761u) >> (32 - 10);  // 10 bits = kPcTable
+}
+
+__device__ __forceinline__ unsigned pc_fhash(int r) {
+  return ((unsigned)r * 0x85ebca6bu) >> (32 - 12);  // 12 bits = 32 * kPcFilterWords
 }
 
 __device__ __forceinline__ int pc_find(const PcBuf& T, int r) {
@@ -177,6 +183,7 @@ __device__ __forceinline__ void pc_produce(const SparseArgs& A, PcBuf& B, int la
     B.col_pre[0] = 0;
     B.m = m;
   }
+  for (int w = lane; w < kPcFilterWords; w += 32) B.filt[w] = 0u;
 
   const int nz = __shfl_sync(0xffffffffu, pre, m - 1);
   // copy: all lanes on one column, 8 columns' loads in flight
@@ -251,7 +258,11 @@ __device__ __forceinline__ void pc_produce(const SparseArgs& A, PcBuf& B, int la
         h = (h + 1) & (kPcTable - 1);
         prev = atomicCAS(&B.key[h], kEmpty, rq[q]);
       }
-      if (prev == kEmpty) own |= 1u << (k0 + q);
+      if (prev == kEmpty) {
+        own |= 1u << (k0 + q);
+        const unsigned fh = pc_fhash(rq[q]);
+        atomicOr(&B.filt[fh >> 5], 1u << (fh & 31));
+      }
       B.slot[e] = (short)h;
     }
   }
@@ -505,7 +516,10 @@ __global__ void __launch_bounds__(64) k_sparse_epoch(SparseArgs A, int W) {
                 }
               }
               hq[q] = pc_hash(rq[q]);
-              kq[q] = rq[q] != kEmpty ? N.key[hq[q]] : kEmpty;
+              // rows the next chunk cannot hold are dropped by its filter
+              const unsigned fh = pc_fhash(rq[q]);
+              const bool maybe = rq[q] != kEmpty && ((N.filt[fh >> 5] >> (fh & 31)) & 1u);
+              kq[q] = maybe ? N.key[hq[q]] : kEmpty;
             }
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
