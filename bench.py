@@ -298,6 +298,8 @@ def _epoch_kernel_name(dp, eng):
         return "k_sparse_epoch"
     if dp.d <= 32:
         return "k_small_epoch"
+    if dp.d <= 16 * 1280:  # csrc/epoch_mid.cu kMidMaxD
+        return "k_mid_epoch"
     if int(lib().syscd_dense_epoch_workspace_bytes(dp.d, eng.n_parts_local)) > 0:
         return "k_grid_epoch"
     return "k_dense_epoch"

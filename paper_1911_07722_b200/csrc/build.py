@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 PKG = os.path.dirname(HERE)
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libsyscd_b200.so")
-SOURCES = ["capi.cu", "plan.cu", "epoch_dense.cu", "epoch_grid.cu", "epoch_small.cu", "epoch_sparse.cu", "exact_logistic.cu", "vecops.cu", "libsvm_io.cu", "epoch_wild.cu"]
+SOURCES = ["capi.cu", "plan.cu", "epoch_dense.cu", "epoch_grid.cu", "epoch_small.cu", "epoch_mid.cu", "epoch_sparse.cu", "exact_logistic.cu", "vecops.cu", "libsvm_io.cu", "epoch_wild.cu"]
 HEADERS = ["common.cuh", "rng.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

@@ -312,6 +312,12 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   return r;
 }
 
+__device__ __forceinline__ uint32_t cluster_nctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+
 __device__ __forceinline__ uint32_t cluster_map(uint32_t local_smem_addr, uint32_t rank) {
   uint32_t out;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(local_smem_addr), "r"(rank));
@@ -334,6 +340,32 @@ __device__ __forceinline__ void cluster_sync_all() {
 
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Worker g of G takes partitions [p_lo, p_hi): contiguous ranges whose
+// boundaries are the partition starts nearest to g*total/G updates, so equal
+// partitions split evenly and no worker is left idle while another holds two.
+__device__ __forceinline__ int64_t nearest_part_start(const int64_t* wp, int n_parts, int64_t t) {
+  int lo = 0, hi = n_parts + 1;  // first index with wp[idx] >= t
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (wp[mid] < t) {
+      lo = mid + 1;
+    } else {
+      hi = mid;
+    }
+  }
+  if (lo > n_parts) lo = n_parts;
+  if (lo > 0 && t - wp[lo - 1] < wp[lo] - t) --lo;
+  return lo;
+}
+
+__device__ __forceinline__ void worker_parts(const int64_t* wp, int n_parts, int G, int g,
+                                             int64_t* p_lo, int64_t* p_hi) {
+  const int64_t total = wp[n_parts];
+  *p_lo = g == 0 ? 0 : nearest_part_start(wp, n_parts, (int64_t)((__int128)total * g / G));
+  *p_hi = g == G - 1 ? n_parts
+                     : nearest_part_start(wp, n_parts, (int64_t)((__int128)total * (g + 1) / G));
 }
 
 __device__ __forceinline__ float warp_sum(float v) {

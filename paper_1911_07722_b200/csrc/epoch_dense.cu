@@ -111,19 +111,6 @@ __host__ __device__ inline SmemLayout smem_layout(int stages, int chunk_rows) {
   return L;
 }
 
-__device__ __forceinline__ int64_t lower_bound_i64(const int64_t* a, int n, int64_t key) {
-  int lo = 0, hi = n;  // first index in [0, n) with a[idx] >= key, or n
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if (a[mid] < key) {
-      lo = mid + 1;
-    } else {
-      hi = mid;
-    }
-  }
-  return lo;
-}
-
 // KIND: the step is compiled in (SYSCD_RIDGE also serves the primal-logistic
 // surrogate, which has the same closed form); the hot loop carries only its
 // own step -- the logistic-dual fp64 Newton would otherwise sit in every
@@ -169,11 +156,8 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
     }
     mbar_init(&xbar[0], 1);
     mbar_init(&xbar[1], 1);
-    const int64_t total = args.wp[args.n_parts];
-    const int64_t t_lo = (int64_t)((__int128)total * g / G);
-    const int64_t t_hi = (int64_t)((__int128)total * (g + 1) / G);
-    int64_t p_lo = g == 0 ? 0 : lower_bound_i64(args.wp, args.n_parts + 1, t_lo);
-    int64_t p_hi = g == G - 1 ? args.n_parts : lower_bound_i64(args.wp, args.n_parts + 1, t_hi);
+    int64_t p_lo, p_hi;
+    worker_parts(args.wp, args.n_parts, G, g, &p_lo, &p_hi);
     if (p_lo > args.n_parts) p_lo = args.n_parts;
     if (p_hi > args.n_parts) p_hi = args.n_parts;
     range[0] = p_lo;
@@ -488,6 +472,8 @@ struct Choice {
 int grid_choose(int64_t d, int* idx, int* G, int* stages, size_t* smem_out);
 int small_workers(int32_t n_parts);
 int small_launch(const syscd_dense_epoch_args* e, cudaStream_t stream);
+bool mid_applicable(int64_t d, int32_t n_parts, int* workers, int* cluster);
+int mid_launch(const syscd_dense_epoch_args* e, cudaStream_t stream);
 constexpr int64_t kSmallMaxD = 32;
 int64_t grid_workspace_bytes(int G);
 int grid_launch(const syscd_dense_epoch_args* e, void* workspace, int64_t ws_bytes,
@@ -566,6 +552,12 @@ extern "C" int syscd_dense_epoch_workers(int64_t d, int32_t n_parts, int32_t* n_
     if (cluster) *cluster = 0;
     return SYSCD_OK;
   }
+  int mw = 0, mc = 0;
+  if (mid_applicable(d, n_parts, &mw, &mc)) {  // chunked-Gram cluster kernel (epoch_mid.cu)
+    *n_workers = mw;
+    if (cluster) *cluster = mc;
+    return SYSCD_OK;
+  }
   Choice ch;
   int st = choose(d, n_parts, &ch);
   if (st) return st;
@@ -576,6 +568,7 @@ extern "C" int syscd_dense_epoch_workers(int64_t d, int32_t n_parts, int32_t* n_
 
 extern "C" int64_t syscd_dense_epoch_workspace_bytes(int64_t d, int32_t n_parts) {
   if (d >= 1 && d <= kSmallMaxD && n_parts >= 1) return 0;
+  if (n_parts >= 1 && mid_applicable(d, n_parts, nullptr, nullptr)) return 0;
   Choice ch;
   if (d < 1 || n_parts < 1 || choose(d, n_parts, &ch) != SYSCD_OK) return -1;
   if (!ch.grid) return 0;
@@ -602,6 +595,13 @@ extern "C" int syscd_dense_epoch(const syscd_dense_epoch_args* e, void* stream) 
       return SYSCD_EINVAL;
     }
     return small_launch(e, (cudaStream_t)stream);
+  }
+  if (mid_applicable(e->d, e->n_parts, nullptr, nullptr)) {
+    if (e->part_ld < e->d) {
+      set_error("syscd_dense_epoch: part_ld < d");
+      return SYSCD_EINVAL;
+    }
+    return mid_launch(e, (cudaStream_t)stream);
   }
   Choice ch;
   int st = choose(e->d, e->n_parts, &ch);

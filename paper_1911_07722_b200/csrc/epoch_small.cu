@@ -67,19 +67,6 @@ __device__ __forceinline__ float small_step(float r, float alpha, float q, float
   }
 }
 
-__device__ __forceinline__ int64_t lb_small(const int64_t* a, int n, int64_t key) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if (a[mid] < key) {
-      lo = mid + 1;
-    } else {
-      hi = mid;
-    }
-  }
-  return lo;
-}
-
 template <int D>
 struct SmallSmem {
   static constexpr int DP = D + 4;  // 16-byte aligned rows, conflict-free 16-byte reads
@@ -117,11 +104,8 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_epoch(SmallArgs A, int 
   __syncthreads();
   const int d = A.d;
   const float a = A.a;
-  const int64_t total = A.wp[A.n_parts];
-  const int64_t t_lo = (int64_t)((__int128)total * g / W);
-  const int64_t t_hi = (int64_t)((__int128)total * (g + 1) / W);
-  const int64_t p_lo = g == 0 ? 0 : lb_small(A.wp, A.n_parts + 1, t_lo);
-  const int64_t p_hi = g == W - 1 ? A.n_parts : lb_small(A.wp, A.n_parts + 1, t_hi);
+  int64_t p_lo, p_hi;
+  worker_parts(A.wp, A.n_parts, W, g, &p_lo, &p_hi);
 
   if (warp > 0) {
     // ------------------------------------------------------------ helpers

@@ -61,19 +61,6 @@ struct SparseArgs {
 
 constexpr int kEmpty = -1;
 
-__device__ __forceinline__ int64_t lb_i64(const int64_t* a, int n, int64_t key) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if (a[mid] < key) {
-      lo = mid + 1;
-    } else {
-      hi = mid;
-    }
-  }
-  return lo;
-}
-
 // tagged replica word: (tag << 32) | fp32 bits; other tags read as zero
 __device__ __forceinline__ float rep_load(const unsigned long long* dv, int64_t r, uint32_t tag) {
   const unsigned long long x = dv[r];
@@ -344,11 +331,8 @@ __global__ void __launch_bounds__(64) k_sparse_epoch(SparseArgs A, int W) {
     fence_mbar_init();
   }
   __syncthreads();
-  const int64_t total = A.wp[A.n_parts];
-  const int64_t t_lo = (int64_t)((__int128)total * g / W);
-  const int64_t t_hi = (int64_t)((__int128)total * (g + 1) / W);
-  const int64_t p_lo = g == 0 ? 0 : lb_i64(A.wp, A.n_parts + 1, t_lo);
-  const int64_t p_hi = g == W - 1 ? A.n_parts : lb_i64(A.wp, A.n_parts + 1, t_hi);
+  int64_t p_lo, p_hi;
+  worker_parts(A.wp, A.n_parts, W, g, &p_lo, &p_hi);
   unsigned long long* dv = A.dv_work + (int64_t)g * A.d;
   const float a = A.a;
   unsigned long long ph[4] = {0, 0, 0, 0};
