@@ -259,39 +259,43 @@ __global__ void __launch_bounds__(kMidBlock, 1) k_mid_epoch(MidArgs A) {
       if (dbg) A.dbg[k * 8 + 1] = clock64();
       const int m = mcount[b];
       const float* tb = tile + (size_t)b * kMidM * rs;
-      // ---- partial c_t and G_ts over this warp's rows on the tensor cores:
-      // D(16 x 24) += X^T(16 x 8) Y(8 x 24) per 8 rows, X = the chunk's
-      // columns, Y = [the chunk's columns | w | 0], mma.m16n8k8 tf32 x 3
-      float acc[3][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      // ---- partial G_ts over this warp's rows on the tensor cores:
+      // D(16 x 16) += X^T(16 x 8) X(8 x 16) per 8 rows (mma.m16n8k8 tf32,
+      // 3 products per tile for fp32 accuracy); c_t = x_t . w with FMAs on
+      // the same A fragments
+      // one accumulator per (n-tile, product): six independent mma chains
+      float acc[2][3][4] = {};
+      float c_lo = 0.f, c_hi = 0.f;  // c for t = gid, gid + 8 (partial over tig)
       {
         const int gid = lane >> 2, tig = lane & 3;
         const float* ra = tb + (size_t)gid * rs;        // rows t = gid, gid + 8
         const float* rb = tb + (size_t)(gid + 8) * rs;
         for (int ks = kw0; ks < kw1; ++ks) {
           const int i0 = ks * 8 + tig;
+          const float x0 = ra[i0], x1 = rb[i0], x2 = ra[i0 + 4], x3 = rb[i0 + 4];
+          const float w0 = wv[i0], w1 = wv[i0 + 4];
+          c_lo = fmaf(x2, w1, fmaf(x0, w0, c_lo));
+          c_hi = fmaf(x3, w1, fmaf(x1, w0, c_hi));
           uint32_t ah[4], al[4];
-          tf32_split(ra[i0], ah[0], al[0]);
-          tf32_split(rb[i0], ah[1], al[1]);
-          tf32_split(ra[i0 + 4], ah[2], al[2]);
-          tf32_split(rb[i0 + 4], ah[3], al[3]);
+          tf32_split(x0, ah[0], al[0]);
+          tf32_split(x1, ah[1], al[1]);
+          tf32_split(x2, ah[2], al[2]);
+          tf32_split(x3, ah[3], al[3]);
           // n-tiles 0, 1: s = gid (+8): the same rows as the A operand
           uint32_t bh0, bl0, bh1, bl1;
           bh0 = ah[0]; bl0 = al[0]; bh1 = ah[2]; bl1 = al[2];
-          mma_tf32(acc[0], ah, bh0, bh1);
-          mma_tf32(acc[0], ah, bl0, bl1);
-          mma_tf32(acc[0], al, bh0, bh1);
+          mma_tf32(acc[0][0], ah, bh0, bh1);
+          mma_tf32(acc[0][1], ah, bl0, bl1);
+          mma_tf32(acc[0][2], al, bh0, bh1);
           bh0 = ah[1]; bl0 = al[1]; bh1 = ah[3]; bl1 = al[3];
-          mma_tf32(acc[1], ah, bh0, bh1);
-          mma_tf32(acc[1], ah, bl0, bl1);
-          mma_tf32(acc[1], al, bh0, bh1);
-          // n-tile 2: column 0 = w, the rest zero
-          const float w0 = gid == 0 ? wv[i0] : 0.f, w1 = gid == 0 ? wv[i0 + 4] : 0.f;
-          tf32_split(w0, bh0, bl0);
-          tf32_split(w1, bh1, bl1);
-          mma_tf32(acc[2], ah, bh0, bh1);
-          mma_tf32(acc[2], ah, bl0, bl1);
-          mma_tf32(acc[2], al, bh0, bh1);
+          mma_tf32(acc[1][0], ah, bh0, bh1);
+          mma_tf32(acc[1][1], ah, bl0, bl1);
+          mma_tf32(acc[1][2], al, bh0, bh1);
         }
+        c_lo += __shfl_xor_sync(0xffffffffu, c_lo, 1);
+        c_lo += __shfl_xor_sync(0xffffffffu, c_lo, 2);
+        c_hi += __shfl_xor_sync(0xffffffffu, c_hi, 1);
+        c_hi += __shfl_xor_sync(0xffffffffu, c_hi, 2);
         // D fragment: rows t = gid, gid + 8; columns 2*tig, 2*tig + 1
         float* wp_w = wpart + warp * kMidG;
 #pragma unroll
@@ -300,11 +304,11 @@ __global__ void __launch_bounds__(kMidBlock, 1) k_mid_epoch(MidArgs A) {
           for (int e = 0; e < 4; ++e) {
             const int t = gid + (e >= 2 ? 8 : 0);
             const int sc = nt * 8 + 2 * tig + (e & 1);
-            if (sc <= t) wp_w[mid_tri(t, sc)] = acc[nt][e];
+            if (sc <= t) wp_w[mid_tri(t, sc)] = acc[nt][0][e] + (acc[nt][1][e] + acc[nt][2][e]);
           }
         if (tig == 0) {
-          wp_w[kMidTri + gid] = acc[2][0];
-          wp_w[kMidTri + gid + 8] = acc[2][2];
+          wp_w[kMidTri + gid] = c_lo;
+          wp_w[kMidTri + gid + 8] = c_hi;
         }
       }
       named_bar_sync(1, kMidThreads);
@@ -378,17 +382,17 @@ __global__ void __launch_bounds__(kMidBlock, 1) k_mid_epoch(MidArgs A) {
       float dl[kMidM];
 #pragma unroll
       for (int t = 0; t < kMidM; ++t) dl[t] = a * delta_s[t];
+      // (columns t >= m of a partial chunk hold finite stale data and delta_t
+      // = 0 there, so no guard: the 16 loads issue back to back)
       for (int gq = tid; gq < ngroups; gq += kMidThreads) {
         float4 w4 = reinterpret_cast<float4*>(wv)[gq];
 #pragma unroll
         for (int t = 0; t < kMidM; ++t) {
-          if (t < m) {
-            const float4 x = reinterpret_cast<const float4*>(tb + (size_t)t * rs)[gq];
-            w4.x = fmaf(dl[t], x.x, w4.x);
-            w4.y = fmaf(dl[t], x.y, w4.y);
-            w4.z = fmaf(dl[t], x.z, w4.z);
-            w4.w = fmaf(dl[t], x.w, w4.w);
-          }
+          const float4 x = reinterpret_cast<const float4*>(tb + (size_t)t * rs)[gq];
+          w4.x = fmaf(dl[t], x.x, w4.x);
+          w4.y = fmaf(dl[t], x.y, w4.y);
+          w4.z = fmaf(dl[t], x.z, w4.z);
+          w4.w = fmaf(dl[t], x.w, w4.w);
         }
         reinterpret_cast<float4*>(wv)[gq] = w4;
       }
