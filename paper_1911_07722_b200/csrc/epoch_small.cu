@@ -133,13 +133,22 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_epoch(SmallArgs A, int 
       float q, alpha;
       int j, m;
     };
-    auto load = [&](const Cursor& c, Staged& st) {
-      st.m = 0;
-      st.j = 0;
+    // ids (the coordinate of each column) of a chunk are loaded one
+    // iteration before its column data, so no load waits on another
+    struct Ids {
+      int j, m;
+    };
+    auto load_ids = [&](const Cursor& c) {
+      Ids id{0, 0};
+      if (valid(c)) id.m = (int)min((int64_t)32, A.wp[c.p + 1] - c.c0);
+      if (lane < kPer && tl < id.m) id.j = A.seq[c.c0 + tl];
+      return id;
+    };
+    auto load = [&](const Ids& id, Staged& st) {
+      st.m = id.m;
+      st.j = id.j;
       st.q = st.alpha = 0.f;
-      if (valid(c)) st.m = (int)min((int64_t)32, A.wp[c.p + 1] - c.c0);
       const bool mine = lane < kPer && tl < st.m;
-      if (mine) st.j = A.seq[c.c0 + tl];
 #pragma unroll
       for (int i = 0; i < kPer; ++i) {
         const int t = hw + kSmallHelpers * i;
@@ -154,9 +163,11 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_epoch(SmallArgs A, int 
     Cursor c_cur{p_lo, p_lo < p_hi ? A.wp[p_lo] - 32 : 0};
     c_cur = advance(c_cur);  // the first non-empty chunk
     Cursor c_nxt = advance(c_cur);
+    Cursor c_nn = advance(c_nxt);
     Staged cur, nxt;
-    load(c_cur, cur);
-    load(c_nxt, nxt);
+    load(load_ids(c_cur), cur);
+    load(load_ids(c_nxt), nxt);
+    Ids id_nn = load_ids(c_nn);
     for (int k = 0; valid(c_cur); ++k) {
       const int b = k & 1;
       const int m = cur.m;
@@ -172,11 +183,14 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_epoch(SmallArgs A, int 
         const int t = hw + kSmallHelpers * i;
         if (t < 32 && lane < D) S.tile[b][t][lane] = cur.col[i];
       }
-      // shift the staging window and put the chunk after next in flight
+      // shift the staging window: the chunk after next goes in flight with
+      // the ids loaded last iteration, the one after that gets its ids
       cur = nxt;
       c_cur = c_nxt;
-      c_nxt = advance(c_nxt);
-      load(c_nxt, nxt);
+      c_nxt = c_nn;
+      load(id_nn, nxt);
+      c_nn = advance(c_nn);
+      id_nn = load_ids(c_nn);
       {
         named_bar_sync(2, 32 * kSmallHelpers);
         // Gram: lane t holds row x_t; this warp fills columns s of G
