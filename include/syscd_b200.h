@@ -93,6 +93,8 @@ typedef struct {
                                       static_node_partition order                 */
   const int64_t* bucket_store_col; /* device: store column of each listed
                                       bucket's first coordinate                   */
+  int64_t* round_updates;          /* optional device array: round_updates[rid] =
+                                      total updates of round rid (NULL: skipped)  */
 } syscd_plan_desc;
 
 /* bytes of workspace syscd_plan needs for n_rounds rounds */

@@ -27,7 +27,7 @@ class PlanDesc(ctypes.Structure):
         ("seed", c_u64), ("n_global", c_i64), ("bucket_size", c_i32), ("n_nodes_local", c_i32),
         ("node0", c_i32), ("P", c_i32), ("T3", c_i32), ("T4", c_i32), ("sampling", c_i32),
         ("repartition", c_i32), ("node_bucket_ptr", ctypes.POINTER(c_i32)),
-        ("node_buckets", c_vp), ("bucket_store_col", c_vp),
+        ("node_buckets", c_vp), ("bucket_store_col", c_vp), ("round_updates", c_vp),
     ]
 
 

@@ -46,6 +46,7 @@ struct PlanParams {
   int32_t* seq;
   int64_t seq_stride;
   int64_t* work_prefix;  // [R][n_parts+1]
+  int64_t* round_updates;  // optional [rid]: total updates of the round
 };
 
 constexpr int kLocalPerm = 64;
@@ -146,7 +147,10 @@ __global__ void k_plan_offsets(PlanParams pp) {
     if (threadIdx.x == 0) carry += total;
     __syncthreads();
   }
-  if (threadIdx.x == 0) wp[pp.n_parts] = carry;
+  if (threadIdx.x == 0) {
+    wp[pp.n_parts] = carry;
+    if (pp.round_updates) pp.round_updates[pp.rid0 + r] = carry;
+  }
 }
 
 __global__ void k_plan_perm(PlanParams pp, int n_rounds) {
@@ -320,6 +324,7 @@ extern "C" int syscd_plan(const syscd_plan_desc* d, int64_t rid0, int32_t n_roun
   pp.seq = seq;
   pp.seq_stride = seq_stride;
   pp.work_prefix = work_prefix;
+  pp.round_updates = d->round_updates;
 
   int nb_max = 0;
   for (int k = 0; k < d->n_nodes_local; ++k)

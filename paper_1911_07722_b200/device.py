@@ -32,8 +32,10 @@ def _ptr(t):
 
 
 def _stream():
-    torch = _torch()
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    """Raw handle of the current CUDA stream (the cheap accessor: this runs
+    several times per round on the host-bound small configs)."""
+    import torch
+    return ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice()))
 
 
 # ---------------------------------------------------------------------------

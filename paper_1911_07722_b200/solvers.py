@@ -24,7 +24,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from ._lib import (DenseEpochArgs, ExactArgs, PlanDesc, SparseEpochArgs, WildEpochArgs, call,
-                   lib)
+                   check, lib)
 from .device import DeviceProblem, Dist, _ptr, _stream, _torch
 from .objective import LOGISTIC, NonFiniteUpdateError
 from .partitioning import DEFAULT_CACHE_LINE_BYTES, default_bucket_size
@@ -185,6 +185,11 @@ class _Engine:
         if self.stride < 0:
             call("syscd_plan_max_updates")
         self.R = max(1, min(cfg.plan_batch, cfg.n_rounds * cfg.T2 if cfg.n_rounds else 1))
+        # per-round update counts, written by the planner (round_updates[rid]);
+        # sized for every round plus the batch planned ahead of the last one
+        self.upd_dev = torch.zeros(max(1, cfg.n_rounds * cfg.T2) + 2 * self.R + 1,
+                                   dtype=torch.int64, device="cuda")
+        self.desc.round_updates = self.upd_dev.data_ptr()
         ws = int(L.syscd_plan_workspace_bytes(ctypes.byref(self.desc), self.R))
         # double-buffered round tables: batch b+1 is planned on a side stream
         # while batch b's epochs run (the permutations are data-independent)
@@ -192,8 +197,6 @@ class _Engine:
                      for _ in range(2)]
         self.cur = 0
         self.side = torch.cuda.Stream()
-        self.upd_dev = torch.zeros(max(1, cfg.n_rounds * cfg.T2 + 1), dtype=torch.int64,
-                                   device="cuda")
         # workers
         d = dp.d
         if dp.storage == "dense":
@@ -226,6 +229,34 @@ class _Engine:
         self.plans_issued = 0      # syscd_plan calls (3 kernel launches each)
         self.launches = 0          # our kernel launches issued (bench accounting)
         dp.grad_into(self.v, self.u)
+        # the per-round hot path reuses one argument struct and raw pointers
+        self._lib = lib()
+        self._workers_for = {}
+        self._p_partials = _ptr(self.partials)
+        self._p_dv = _ptr(self.dv)
+        self._p_v = _ptr(self.v)
+        self._p_u = _ptr(self.u)
+        self._p_y = _ptr(dp.y)
+        if dp.storage == "dense":
+            e = DenseEpochArgs()
+            e.kind = dp.kind
+            e.d = dp.d
+            e.lda = dp.lda
+            e.A = dp.At.data_ptr()
+            e.sq = dp.sq.data_ptr()
+            e.alpha = self.alpha.data_ptr()
+            e.a = self.a
+            e.lam = dp.lam
+            e.n_coords = dp.n_coords
+            e.iid = 1 if cfg.sampling == "iid" else 0
+            e.n_store = dp.n_store
+            e.partials = self.partials.data_ptr()
+            e.part_ld = self.part_ld
+            e.status = self.status.data_ptr()
+            e.workspace = self.epoch_ws.data_ptr()
+            e.workspace_bytes = self.epoch_ws.numel()
+            self._dargs = e
+            self._dargs_ref = ctypes.byref(e)
 
     @staticmethod
     def _dense_workers(d, n_parts):
@@ -236,6 +267,14 @@ class _Engine:
 
     # -- one device round (rid) over node range [k0, k1) with lin_vec u -------
     def _plan(self, buf, rid0, stream):
+        if rid0 + self.R > self.upd_dev.numel():
+            # more rounds than configured (rare): grow the count table once
+            self.torch.cuda.synchronize()
+            grown = self.torch.zeros(2 * (rid0 + self.R), dtype=self.torch.int64, device="cuda")
+            grown[:self.upd_dev.numel()].copy_(self.upd_dev)
+            self.torch.cuda.synchronize()
+            self.upd_dev = grown
+            self.desc.round_updates = grown.data_ptr()
         call("syscd_plan", ctypes.byref(self.desc), int(rid0), self.R, _ptr(buf.seq), self.stride,
              _ptr(buf.wp), _ptr(buf.ws), buf.ws.numel(), ctypes.c_void_p(stream.cuda_stream))
         buf.lo, buf.hi = rid0, rid0 + self.R
@@ -263,6 +302,12 @@ class _Engine:
         self._plan(cur, nxt.hi, self.side)
         return nxt, rid - nxt.lo
 
+    def round_ptrs(self, rid):
+        """Raw device pointers of round rid's seq and work_prefix rows."""
+        buf, r = self._ensure_plan(rid)
+        return (buf.seq_ptr + 4 * r * self.stride,
+                buf.wp_ptr + 8 * r * (self.n_parts_local + 1))
+
     def round_tables(self, rid):
         buf, r = self._ensure_plan(rid)
         seq = buf.seq[r * self.stride:]
@@ -274,46 +319,26 @@ class _Engine:
         lin_vec u; leaves their summed replicas in self.dv."""
         cfg, dp = self.cfg, self.dp
         node_hi = self.K_local if node_hi is None else node_hi
-        seq, wp = self.round_tables(rid)
-        if node_lo == 0:
-            if rid >= self.upd_dev.numel():
-                grown = self.torch.zeros(2 * rid + 2, dtype=self.torch.int64, device="cuda")
-                grown[:self.upd_dev.numel()].copy_(self.upd_dev)
-                self.upd_dev = grown
-            self.upd_dev[rid:rid + 1].copy_(wp[self.n_parts_local:self.n_parts_local + 1])
+        seq_ptr, wp_ptr = self.round_ptrs(rid)
         p0 = node_lo * cfg.P
         nparts = (node_hi - node_lo) * cfg.P
-        wp_ptr = ctypes.c_void_p(wp.data_ptr() + 8 * p0)
+        stream = _stream()
         if dp.storage == "dense":
-            e = DenseEpochArgs()
-            e.kind = dp.kind
-            e.d = dp.d
-            e.lda = dp.lda
-            e.A = dp.At.data_ptr()
-            e.sq = dp.sq.data_ptr()
-            e.alpha = self.alpha.data_ptr()
+            e = self._dargs
             e.u = u.data_ptr()
-            e.seq = seq.data_ptr()
-            e.work_prefix = wp_ptr.value
+            e.seq = seq_ptr
+            e.work_prefix = wp_ptr + 8 * p0
             e.n_parts = nparts
-            e.a = self.a
-            e.lam = dp.lam
-            e.n_coords = dp.n_coords
-            e.iid = 1 if cfg.sampling == "iid" else 0
-            e.n_store = dp.n_store
-            e.partials = self.partials.data_ptr()
-            e.part_ld = self.part_ld
-            e.status = self.status.data_ptr()
-            e.workspace = self.epoch_ws.data_ptr()
-            e.workspace_bytes = self.epoch_ws.numel()
             if self.kernel_events is not None:
                 self.kernel_events[0].record()
-            call("syscd_dense_epoch", ctypes.byref(e), _stream())
+            check(self._lib.syscd_dense_epoch(self._dargs_ref, stream), "syscd_dense_epoch")
             if self.kernel_events is not None:
                 self.kernel_events[1].record()
-            nw = self._dense_workers(dp.d, nparts)[0]
-            call("syscd_reduce_partials", _ptr(self.partials), self.part_ld, nw, dp.d,
-                 _ptr(self.dv), _stream())
+            nw = self._workers_for.get(nparts)
+            if nw is None:
+                nw = self._workers_for[nparts] = self._dense_workers(dp.d, nparts)[0]
+            check(self._lib.syscd_reduce_partials(self._p_partials, self.part_ld, nw, dp.d,
+                                                  self._p_dv, stream), "syscd_reduce_partials")
         else:
             cp, ri, va = dp.csc
             e = SparseEpochArgs()
@@ -325,8 +350,8 @@ class _Engine:
             e.sq = dp.sq.data_ptr()
             e.alpha = self.alpha.data_ptr()
             e.u = u.data_ptr()
-            e.seq = seq.data_ptr()
-            e.work_prefix = wp_ptr.value
+            e.seq = seq_ptr
+            e.work_prefix = wp_ptr + 8 * p0
             e.n_parts = nparts
             e.a = self.a
             e.lam = dp.lam
@@ -351,11 +376,6 @@ class _Engine:
         """K=P=1 primal logistic round: exact updates on the live v."""
         dp = self.dp
         seq, wp = self.round_tables(rid)
-        if rid >= self.upd_dev.numel():
-            grown = self.torch.zeros(2 * rid + 2, dtype=self.torch.int64, device="cuda")
-            grown[:self.upd_dev.numel()].copy_(self.upd_dev)
-            self.upd_dev = grown
-        self.upd_dev[rid:rid + 1].copy_(wp[1:2])
         e = ExactArgs()
         e.d = dp.d
         if dp.storage == "dense":
@@ -384,9 +404,11 @@ class _Engine:
             return
         if cfg.T2 == 1:
             self.epoch(t1, self.u)
-            self.dist.allreduce_(self.dv)
-            call("syscd_apply_dv", dp.kind, dp.d, _ptr(self.dv), _ptr(self.v), _ptr(dp.y),
-                 dp.lam, dp.n_coords, _ptr(self.u), _stream())
+            if self.dist.world > 1:
+                self.dist.allreduce_(self.dv)
+            check(self._lib.syscd_apply_dv(dp.kind, dp.d, self._p_dv, self._p_v, self._p_y,
+                                           dp.lam, dp.n_coords, self._p_u, _stream()),
+                  "syscd_apply_dv")
             return
         # T2 > 1: node-local rounds with the drift term (solvers.py:373-398)
         drift = cfg.K * dp.gamma
@@ -440,6 +462,8 @@ class _PlanBuf:
     def __init__(self, torch, R, stride, n_parts, ws_bytes):
         self.seq = torch.empty(R * max(1, stride), dtype=torch.int32, device="cuda")
         self.wp = torch.empty(R * (n_parts + 1), dtype=torch.int64, device="cuda")
+        self.seq_ptr = self.seq.data_ptr()
+        self.wp_ptr = self.wp.data_ptr()
         self.ws = torch.empty(max(ws_bytes, 256), dtype=torch.uint8, device="cuda")
         self.lo = self.hi = None
         self.ready = torch.cuda.Event()
