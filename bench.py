@@ -181,8 +181,8 @@ def run_ours(args):
         t = args.warmup + s
         eng.kernel_events = (k_start[s], k_stop[s])
         eng.global_round(t)
-    # per round: epoch + reduce + apply (+ the per-round update-count copy is a
-    # cudaMemcpyAsync, not a kernel); per plan batch: 3 planning kernels
+    # per round: epoch + reduce + apply; per plan batch: 3 planning kernels
+    # (which also write the per-round update counts)
     launches = 3 * args.steps + 3 * (eng.plans_issued - plans0)
     stop.record()
     torch.cuda.synchronize()
@@ -437,6 +437,8 @@ def e2e_run(args, wl, world, dist):
         _ = res.alpha.sum()
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
+        if os.environ.get("SYSCD_BENCH_DEBUG"):
+            print(f"e2e step {s}: {1e3 * dt:.2f} ms", file=sys.stderr)
         if s > 0:
             times.append(dt)
             upd += res.total_updates
