@@ -50,6 +50,11 @@ CASES = [
     (2, 0.5, dict(K=1, P=1, bucket_size=8, T1=3)),
     (2, 0.5, dict(K=1, P=3, bucket_size=4, T1=2)),
     (4, 0.0002, dict(K=2, P=3, bucket_size=16, sampling="iid", T3=3, T4=4, T1=3)),
+    # cluster regime (d > 20480, several partitions): k_dense_gram_epoch
+    (2, 0.1, dict(K=1, P=8, bucket_size=4, T1=3)),
+    (2, 0.25, dict(K=1, P=16, bucket_size=3, T1=2)),
+    (2, 0.1, dict(K=1, P=6, bucket_size=5, sampling="iid", T3=4, T4=6, T1=2)),
+    (3, 0.05, dict(K=2, P=4, bucket_size=8, T1=2)),
     # iid on the grid-wide kernel: repeats inside the prefetch window
     (3, 0.15, dict(K=1, P=1, bucket_size=8, sampling="iid", T3=12, T4=8, T1=3)),
     (2, 0.5, dict(K=1, P=2, bucket_size=4, sampling="iid", T3=20, T4=6, T1=2)),
@@ -266,6 +271,8 @@ def _edge_pair(kind, d, n, seed, zero_cols=(), lam=None):
     (31, 40, dict(K=2, P=2, bucket_size=4)),        # small-d kernel, K > 1 on one GPU
     (33, 40, dict(K=1, P=4, bucket_size=4)),        # just above the small-d threshold
     (600, 50, dict(K=1, P=5, bucket_size=3, sampling="iid", T3=2, T4=4)),
+    (30011, 48, dict(K=1, P=4, bucket_size=4)),     # cluster kernel, ragged last CTA
+    (52003, 37, dict(K=1, P=5, bucket_size=3, sampling="iid", T3=2, T4=5)),
 ])
 def test_edge_geometries(cuda, kind, d, n, kw):
     from paper_1911_07722_b200 import SolverConfig, run_syscd
