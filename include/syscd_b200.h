@@ -119,7 +119,9 @@ typedef struct {
   const float* A;          /* device, store columns                                 */
   const float* sq;         /* device, column squared norms per store column         */
   float* alpha;            /* device, model per store column (read/write)           */
-  const float* u;          /* device, lin_vec = grad f(v) (+ drift), length d       */
+  const float* u;          /* device, lin_vec = grad f(v) (+ drift), length d, 16-B
+                              aligned and readable up to round_up(d, 4) (bulk copies
+                              move 16-byte multiples; the padding is ignored)       */
   const int32_t* seq;      /* device, one round of syscd_plan output                */
   const int64_t* work_prefix; /* device, [n_parts+1]                                */
   int32_t n_parts;

@@ -187,8 +187,13 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
   if (warp == NWC) {
     // ------------------------------------------------------------ producer
     const uint64_t policy = args.evict_first ? policy_evict_first() : policy_evict_last();
+    const uint64_t upolicy = policy_evict_last();
     uint32_t stage = 0, phase = 0;
     int jreg = 0;
+    int64_t ppart = p_lo;
+    while (ppart < p_hi && args.wp[ppart + 1] <= s_begin) ++ppart;
+    int64_t ppart_end = ppart < p_hi ? args.wp[ppart + 1] : s_end;
+    const float* uslice = args.u + row0;
     for (int64_t s = s_begin; s < s_end; ++s) {
       const int64_t rel = s - s_begin;
       if ((rel & 31) == 0) {
@@ -196,6 +201,12 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
         jreg = q < s_end ? args.seq[q] : 0;
       }
       const int j = __shfl_sync(0xffffffffu, jreg, (int)(rel & 31));
+      const bool part_last = s + 1 == ppart_end;
+      if (part_last) {
+        ++ppart;
+        while (ppart < p_hi && args.wp[ppart + 1] <= s + 1) ++ppart;
+        ppart_end = ppart < p_hi ? args.wp[ppart + 1] : s_end;
+      }
       if (lane == 0) {
         const float* col = args.A + (int64_t)j * args.lda + row0;
         // perm mode: alpha_j is only written by this cluster, at this step,
@@ -219,6 +230,26 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
           if (++stage == (uint32_t)S) {
             stage = 0;
             phase ^= 1u;
+          }
+        }
+        if (part_last) {
+          // the partition-end flush reads u through the ring too (u is
+          // L2-resident; staging it turns the flush into one shared-memory pass)
+#pragma unroll 1
+          for (int c = 0; c < NCH; ++c) {
+            mbar_wait(&empty[stage], phase ^ 1u);
+            const uint32_t bytes = chunk_bytes[c];
+            if (bytes) {
+              mbar_arrive_expect_tx(&full[stage], bytes);
+              tma_load_1d(ring + (size_t)stage * CHUNK, uslice + c * CHUNK, bytes, &full[stage],
+                          upolicy);
+            } else {
+              mbar_arrive(&full[stage]);
+            }
+            if (++stage == (uint32_t)S) {
+              stage = 0;
+              phase ^= 1u;
+            }
           }
         }
       }
@@ -334,38 +365,33 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
         // fold this partition's replica (w - u)/a into the cluster's partial
         // sum: plain store for the first partition, then fire-and-forget
         // red.global.add (same thread, same address: applied in program
-        // order, so the sum stays deterministic); u comes through the
-        // read-only path so the loads issue back to back.
-        // u loads are pipelined one chunk ahead (a compiler barrier keeps
-        // ptxas from hoisting all R of them, which would spill the replica)
-        float ucur[RC], unxt[RC];
-#pragma unroll
-        for (int k = 0; k < RC; ++k) ucur[k] = k < qmax ? __ldg(ub + k * NTC) : 0.f;
+        // order, so the sum stays deterministic); the producer staged this
+        // CTA's slice of u into the ring right after the partition's last
+        // column, so the flush is one shared-memory pass.
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
-          if (c + 1 < NCH) {
-#pragma unroll
-            for (int k = 0; k < RC; ++k) {
-              const int q = (c + 1) * RC + k;
-              unxt[k] = q < qmax ? __ldg(ub + q * NTC) : 0.f;
-            }
-          }
-          asm volatile("" ::: "memory");
+          mbar_wait(&full[stage0], phase0);
+          const float* uu = ring_t + (size_t)stage0 * CHUNK;
 #pragma unroll
           for (int k = 0; k < RC; ++k) {
             const int q = c * RC + k;
             if (q < qmax) {
-              const float dv = (w[q] - ucur[k]) * inv_a;
+              const float uv = uu[k * NTC];
+              const float dv = (w[q] - uv) * inv_a;
               if (flushed) {
                 red_add_f32(out + q * NTC, dv);
               } else {
                 out[q * NTC] = dv;
               }
-              w[q] = ucur[k];
+              w[q] = uv;
             }
           }
-#pragma unroll
-          for (int k = 0; k < RC; ++k) ucur[k] = unxt[k];
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[stage0]);
+          if (++stage0 == (uint32_t)S) {
+            stage0 = 0;
+            phase0 ^= 1u;
+          }
         }
         flushed = true;
         ++part;
