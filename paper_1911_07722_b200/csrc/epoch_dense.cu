@@ -218,7 +218,8 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
           mbar_wait(&empty[stage], phase ^ 1u);
           if (c == 0)
             meta[s & (kMetaRing - 1)] =
-                make_int4(j, __float_as_int(aj), __float_as_int(qj),
+                make_int4(part_last ? (int)((unsigned)j | 0x80000000u) : j, __float_as_int(aj),
+                          __float_as_int(qj),
                           __float_as_int(step_inv(args.kind, args.a, qj, args.lam_f)));
           const uint32_t bytes = chunk_bytes[c];
           if (bytes) {
@@ -239,6 +240,8 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
           for (int c = 0; c < NCH; ++c) {
             mbar_wait(&empty[stage], phase ^ 1u);
             const uint32_t bytes = chunk_bytes[c];
+            if (args.dbg != nullptr && blockIdx.x == 0 && s - s_begin < 512)
+              args.dbg[7168 + (s - s_begin) * 8 + c] = gtimer();
             if (bytes) {
               mbar_arrive_expect_tx(&full[stage], bytes);
               tma_load_1d(ring + (size_t)stage * CHUNK, uslice + c * CHUNK, bytes, &full[stage],
@@ -269,9 +272,6 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
     const float inv_a = (float)(1.0 / args.a_d);
     float* out = args.partials + (int64_t)g * args.part_ld + row0 + tid;
     bool flushed = false;
-    int64_t part = p_lo;
-    while (part < p_hi && args.wp[part + 1] <= s_begin) ++part;
-    int64_t part_end = part < p_hi ? args.wp[part + 1] : s_end;
     uint32_t stage0 = 0, phase0 = 0;  // ring position of the current step's chunk 0
     // exchange addresses: slot[buf][rank] and xbar[buf] in peer `lane`
     uint32_t peer_slot = 0, peer_bar = 0;
@@ -308,7 +308,8 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
       }
       if (dbg && t < 512) args.dbg[t * 6 + 1] = gtimer();
       const int4 mt = meta[s & (kMetaRing - 1)];
-      const int j = mt.x;
+      const int j = mt.x & 0x7fffffff;
+      const bool part_last = mt.x < 0;  // the producer marks a partition's last column
       float aj = __int_as_float(mt.y);
       const float qj = __int_as_float(mt.z);
       float acc = warp_sum(acc0 + acc1);
@@ -361,7 +362,7 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
         }
       }
       if (dbg && t < 512) args.dbg[t * 6 + 5] = gtimer();
-      if (s + 1 == part_end) {
+      if (part_last) {
         // fold this partition's replica (w - u)/a into the cluster's partial
         // sum: plain store for the first partition, then fire-and-forget
         // red.global.add (same thread, same address: applied in program
@@ -371,21 +372,38 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
           mbar_wait(&full[stage0], phase0);
+          if (dbg && t < 512) args.dbg[3072 + t * 8 + c] = gtimer();
           const float* uu = ring_t + (size_t)stage0 * CHUNK;
+          float uv[RC];
 #pragma unroll
-          for (int k = 0; k < RC; ++k) {
-            const int q = c * RC + k;
-            if (q < qmax) {
-              const float uv = uu[k * NTC];
-              const float dv = (w[q] - uv) * inv_a;
-              if (flushed) {
-                red_add_f32(out + q * NTC, dv);
-              } else {
-                out[q * NTC] = dv;
+          for (int k = 0; k < RC; ++k) uv[k] = uu[k * NTC];  // rows past d read 0
+          // branch-free body for whole chunks, so the loads and reds batch
+          if (c * RC + RC <= qmax) {
+            if (flushed) {
+#pragma unroll
+              for (int k = 0; k < RC; ++k)
+                red_add_f32(out + (c * RC + k) * NTC, (w[c * RC + k] - uv[k]) * inv_a);
+            } else {
+#pragma unroll
+              for (int k = 0; k < RC; ++k)
+                out[(c * RC + k) * NTC] = (w[c * RC + k] - uv[k]) * inv_a;
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < RC; ++k) {
+              const int q = c * RC + k;
+              if (q < qmax) {
+                const float dv = (w[q] - uv[k]) * inv_a;
+                if (flushed) {
+                  red_add_f32(out + q * NTC, dv);
+                } else {
+                  out[q * NTC] = dv;
+                }
               }
-              w[q] = uv;
             }
           }
+#pragma unroll
+          for (int k = 0; k < RC; ++k) w[c * RC + k] = uv[k];
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[stage0]);
           if (++stage0 == (uint32_t)S) {
@@ -394,9 +412,7 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
           }
         }
         flushed = true;
-        ++part;
-        while (part < p_hi && args.wp[part + 1] <= s + 1) ++part;
-        part_end = part < p_hi ? args.wp[part + 1] : s_end;
+        if (dbg && t < 512) args.dbg[3072 + t * 8 + 7] = gtimer();
       }
     }
     if (!flushed) {
@@ -562,9 +578,10 @@ using namespace syscd;
 
 static void* g_dbg_buffer = nullptr;
 // Debug hook (not part of the header ABI): when set to a device buffer of
-// >= 512*6 uint64, the next dense epochs record SM clock cycles at the step
+// >= 512*8 uint64, the next dense epochs record SM clock cycles at the step
 // phases of CTA 0 (start, dot done, CTA reduce done, exchange done, step
-// done, axpy done).
+// done, axpy done; at [3072 + 2t]: partition-end flush, first u chunk ready
+// and flush done).
 extern "C" void syscd_debug_set_timeline(void* device_buffer) { g_dbg_buffer = device_buffer; }
 
 extern "C" int syscd_dense_epoch_workers(int64_t d, int32_t n_parts, int32_t* n_workers,

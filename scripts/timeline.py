@@ -12,13 +12,16 @@ wl = workload(cfg_id)
 eng = _Engine(wl.problem, wl.solver, Dist())
 for t in range(3):
     eng.global_round(t)
-buf = torch.zeros(512 * 6, dtype=torch.int64, device="cuda")
+buf = torch.zeros(512 * 22, dtype=torch.int64, device="cuda")
 L = lib(); L.syscd_debug_set_timeline.argtypes = [ctypes.c_void_p]
 L.syscd_debug_set_timeline(buf.data_ptr())
 eng.global_round(3)
 torch.cuda.synchronize()
 L.syscd_debug_set_timeline(None)
-t = buf.view(512, 6).cpu().numpy().astype(np.float64)
+raw = buf.cpu().numpy().astype(np.float64)
+t = raw[:3072].reshape(512, 6)
+fl = raw[3072:7168].reshape(512, 8)
+pu = raw[7168:].reshape(512, 8)
 t = t[t[:, 0] > 0] / 1.965  # SM cycles -> ns at the 1965 MHz boost clock
 d = np.diff(t, axis=1)
 step = np.diff(t[:, 0])
@@ -28,3 +31,11 @@ for i, nm in enumerate(names):
     print(f"  {nm:18s} mean {d[:, i].mean():7.0f} ns  median {np.median(d[:, i]):7.0f}  p90 {np.percentile(d[:, i], 90):7.0f}")
 tail = t[1:, 0] - t[:-1, 5]
 print(f"  {'flush/loop':18s} mean {tail.mean():7.0f} ns  median {np.median(tail):7.0f}  max {tail.max():7.0f}")
+fi = np.nonzero(fl[:len(t), 0] > 0)[0]
+if len(fi):
+    base = t[fi, 5] * 1.965
+    for c in range(6):
+        print(f"  flush chunk {c} ready at +{((fl[fi, c] - base) / 1.965).mean():.0f} ns")
+    print(f"  flush done at +{((fl[fi, 7] - base) / 1.965).mean():.0f} ns ({len(fi)} flushes)")
+    for c in range(6):
+        print(f"  u chunk {c} wait begins at +{((pu[fi, c] - base) / 1.965).mean():.0f} ns")
