@@ -13,7 +13,10 @@ import os
 from .objective import NonFiniteUpdateError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsyscd_b200.so")
+# SYSCD_TRACE=1 selects the instrumented build (per-event %globaltimer stamps,
+# scripts/timeline*.py only); the product is always libsyscd_b200.so
+LIB_PATH = os.path.join(_HERE, "libsyscd_b200_trace.so" if os.environ.get("SYSCD_TRACE")
+                        else os.environ.get("SYSCD_LIB_NAME", "libsyscd_b200.so"))
 
 SYSCD_OK, SYSCD_EINVAL, SYSCD_ENONFINITE, SYSCD_ECUDA = 0, 1, 2, 3
 RIDGE, LOGISTIC, LASSO, SVM_DUAL, LOGISTIC_DUAL = 0, 1, 2, 3, 4

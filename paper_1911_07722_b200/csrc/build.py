@@ -11,7 +11,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 PKG = os.path.dirname(HERE)
 ROOT = os.path.dirname(PKG)
-LIB = os.path.join(PKG, "libsyscd_b200.so")
+TRACE = bool(os.environ.get("SYSCD_TRACE"))
+LIB = os.path.join(PKG, "libsyscd_b200_trace.so" if TRACE else
+                   os.environ.get("SYSCD_LIB_NAME", "libsyscd_b200.so"))
 SOURCES = ["capi.cu", "plan.cu", "epoch_dense.cu", "epoch_grid.cu", "epoch_small.cu", "epoch_mid.cu", "epoch_sparse.cu", "exact_logistic.cu", "vecops.cu", "libsvm_io.cu", "epoch_wild.cu"]
 HEADERS = ["common.cuh", "rng.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -19,7 +21,7 @@ FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
     "--expt-relaxed-constexpr", "-Xptxas", "-v",
-]
+] + (["-DSYSCD_TRACE"] if TRACE else []) + os.environ.get("SYSCD_NVCC_DEFS", "").split()
 
 
 def _stale():
@@ -35,18 +37,33 @@ def _stale():
 def build(force=False, verbose=False):
     if not force and not _stale():
         return LIB
-    objdir = os.path.join(HERE, "_obj")
+    objdir = os.path.join(HERE, "_obj_trace" if TRACE else "_obj")
+    if os.environ.get("SYSCD_NVCC_DEFS"):  # experiment variants build in their own tree
+        objdir = os.path.join(HERE, "_obj_" + os.path.basename(LIB).replace(".so", ""))
     os.makedirs(objdir, exist_ok=True)
-    objs = []
-    for src in SOURCES:
+    hdr_t = max(os.path.getmtime(p) for p in
+                [os.path.join(HERE, h) for h in HEADERS]
+                + [os.path.join(ROOT, "include", "syscd_b200.h"), os.path.abspath(__file__)])
+
+    def compile_one(src):
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-c", os.path.join(HERE, src), "-o", obj]
+        srcp = os.path.join(HERE, src)
+        if (not force and os.path.exists(obj)
+                and os.path.getmtime(obj) > max(os.path.getmtime(srcp), hdr_t)):
+            return obj, ""
+        cmd = [NVCC, *FLAGS, "-c", srcp, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
-        if verbose:
-            sys.stderr.write(r.stderr)
-        objs.append(obj)
+        return obj, r.stderr
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    objs = [o for o, _ in results]
+    if verbose:
+        for _, err in results:
+            sys.stderr.write(err)
     tmp = LIB + ".tmp"
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", tmp,
            "-lcudart"]

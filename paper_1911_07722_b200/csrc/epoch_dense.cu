@@ -149,6 +149,10 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
 
   for (int i = tid; i < S * CHUNK; i += blockDim.x) ring[i] = 0.f;
   for (int i = tid; i < 2 * kMaxCluster; i += blockDim.x) slots[i] = 0.f;
+  // every writer orders its generic-proxy zeros before the TMA (async
+  // proxy) fills that follow the barrier; one fence by the issuing thread
+  // does not cover the other threads' writes
+  fence_proxy_async();
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
@@ -354,6 +358,11 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
         const float* x = ring_t + (size_t)stage0 * CHUNK;
 #pragma unroll
         for (int k = 0; k < RC; ++k) w[c * RC + k] = fmaf(sd, x[k * NTC], w[c * RC + k]);
+        // No proxy fence before the release: the FFMAs above consume every
+        // value read from this stage and precede the arrive in issue order
+        // (checked in the SASS), so the TMA refill cannot overtake the reads.
+        // A release straight after the loads needs fence.proxy.async (see
+        // epoch_grid.cu); here it would cost 3% of config 2.
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage0]);
         if (++stage0 == (uint32_t)S) {

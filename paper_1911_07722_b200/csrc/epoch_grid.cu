@@ -45,6 +45,13 @@ constexpr int kGMeta = 64;  // metadata ring (columns)
 constexpr int kGTot = 8;    // totals ring in shared memory (events), > LL+1
 constexpr int kGVal = 32;   // max values per event record
 constexpr int kGRecent = 64;  // iid: recently resolved (j, alpha) per math warp, >= prefetch lead
+constexpr int kGRed = 8;      // CTA-reduction slots (events)
+#ifndef SYSCD_GRID_RSLOTS
+#define SYSCD_GRID_RSLOTS 1  // events in flight per reducer warp (2: no gain measured)
+#endif
+#ifndef SYSCD_GRID_SLEEP
+#define SYSCD_GRID_SLEEP 256  // reducer poll back-off (ns)
+#endif
 
 struct GridArgs {
   const float* A;
@@ -82,7 +89,7 @@ struct GridSmem {
 
 __host__ __device__ inline size_t galign(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-__host__ __device__ inline GridSmem grid_smem(int stages, int cta_rows) {
+__host__ __device__ inline GridSmem grid_smem(int stages, int cta_rows, int ns) {
   GridSmem L;
   L.ring = 0;
   size_t o = galign((size_t)stages * cta_rows * 4, 128);
@@ -96,7 +103,7 @@ __host__ __device__ inline GridSmem grid_smem(int stages, int cta_rows) {
   L.tot = o;
   o += kGTot * kGVal * 4;
   L.red = o;
-  o += 2 * 16 * kGVal * 4;
+  o += (size_t)kGRed * 16 * ns * 4;
   o = galign(o, 16);
   L.meta = o;
   o += kGMeta * 16;
@@ -118,6 +125,53 @@ __device__ __forceinline__ unsigned long long ld_tagged(const unsigned long long
   return w;
 }
 
+// Sum NV values (NV a power of two <= 32) over a warp with log2(NV) halving
+// exchanges followed by the remaining butterfly: NV-1 + 5-log2(NV) shuffles
+// instead of 5*NV.  On return v[0] of lane l holds the warp total of value
+// multi_index<NV>(l) (identical in every lane of an aligned group of 32/NV).
+template <int NV>
+__device__ __forceinline__ float warp_sum_multi(float (&v)[NV], int lane) {
+  int cnt = NV;
+  int off = 16;
+#pragma unroll
+  for (int step = 0; step < 5; ++step) {
+    if (cnt > 1) {
+      const int half = cnt / 2;
+      const bool upper = (lane & off) != 0;
+#pragma unroll
+      for (int k = 0; k < NV / 2; ++k) {
+        if (k < half) {
+          const float send = upper ? v[k] : v[k + half];
+          const float keep = upper ? v[k + half] : v[k];
+          v[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+      }
+      cnt = half;
+    } else {
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
+    }
+    off >>= 1;
+  }
+  return v[0];
+}
+
+template <int NV>
+__host__ __device__ constexpr int multi_index(int lane) {
+  int idx = 0, cnt = NV, off = 16;
+  for (int step = 0; step < 5 && cnt > 1; ++step) {
+    cnt /= 2;
+    if (lane & off) idx += cnt;
+    off >>= 1;
+  }
+  return idx;
+}
+
+__host__ __device__ constexpr int pow2_at_least(int x) {
+  int p = 1;
+  while (p < x) p *= 2;
+  return p;
+}
+
 template <int BB, int LL>
 struct GridLayout {
   static constexpr int kS = 0;
@@ -130,7 +184,10 @@ struct GridLayout {
   }
 };
 
-template <int RR, int BB, int LL>
+// LDUAL: the logistic-dual instance (the fp64 Newton is compiled only into
+// it); the closed-form steps (ridge / primal logistic, lasso, svm dual) share
+// the other instance.
+template <int RR, int BB, int LL, bool LDUAL>
 __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
   constexpr int NTC = 416;  // 13 math warps + producer + 2 reducers = 16 warps
   constexpr int NWC = NTC / 32;
@@ -138,11 +195,18 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
   using Lay = GridLayout<BB, LL>;
   constexpr int NS = Lay::kNS;
   static_assert(NS <= kGVal, "event record too large");
+  constexpr int NP = pow2_at_least(NS);
   constexpr int CTA_ROWS = NTC * RR;
+  // record layout of one event: CTA-major (word cta * NS + c), so one CTA's
+  // NS words share a 32-byte sector and few CTAs write into one L2 line.
+  // (The component-major layout c * G + cta put 16 writers on every line and
+  // every reducer's polls on the same few lines: config 3 ran at 12-18 ms per
+  // epoch instead of 8.3, depending on how the CTAs happened to convoy.)
+#define GREC_IDX(c, cta_) ((size_t)(cta_) * NS + (c))
 
   extern __shared__ __align__(128) unsigned char smem[];
   const int S = A.stages;
-  const GridSmem Lo = grid_smem(S, CTA_ROWS);
+  const GridSmem Lo = grid_smem(S, CTA_ROWS, NS);
   float* ring = reinterpret_cast<float*>(smem + Lo.ring);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Lo.full);
   uint64_t* empty = reinterpret_cast<uint64_t*>(smem + Lo.empty);
@@ -163,6 +227,10 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
   const int64_t s_end = A.wp[A.n_parts];
 
   for (int i = tid; i < S * CTA_ROWS; i += blockDim.x) ring[i] = 0.f;
+  // every writer orders its generic-proxy zeros before the TMA (async
+  // proxy) fills that follow the barrier; one fence by the issuing thread
+  // does not cover the other threads' writes
+  fence_proxy_async();
   for (int i = tid; i < 16 * kGRecent; i += blockDim.x) recent[i] = make_int2(-1, 0);
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
@@ -220,42 +288,69 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
     constexpr int NQ = 5;  // ceil(148 / 32) CTAs per lane
     int64_t events = 0;
     for (int p = 0; p < A.n_parts; ++p) events += (A.wp[p + 1] - A.wp[p] + BB - 1) / BB;
-    for (int64_t r = warp - NWC - 1; r < events; r += 2) {
-      const unsigned long long* rec = A.recs + (size_t)(r % kGNB) * NS * G;
-      const uint32_t tag = (uint32_t)(r + 1);
-      unsigned long long wv[NS][NQ];
-      bool done;
-      do {
+    // Each reducer warp keeps RSL events in flight (warp w, slot k takes
+    // events r = w + 2k (mod 2*RSL), in order per slot): a slot whose event is
+    // complete sums it and hands it over while the other slots keep polling,
+    // so the totals of consecutive events are gathered concurrently.  A word
+    // carrying its event's tag is final: later polls reload only the words
+    // still missing (the records of the CTAs that are behind).
+    constexpr int RSL = NS <= 4 ? SYSCD_GRID_RSLOTS : 1;  // registers: RSL*NS*NQ words
+    int64_t rs_ev[RSL];
+    unsigned long long wv[RSL][NS][NQ];
 #pragma unroll
-        for (int k = 0; k < NS; ++k)
+    for (int k = 0; k < RSL; ++k) {
+      rs_ev[k] = (warp - NWC - 1) + 2 * k;
+#pragma unroll
+      for (int c = 0; c < NS; ++c)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) wv[k][c][q] = 0ull;
+    }
+    for (;;) {
+      bool any = false, progressed = false;
+#pragma unroll
+      for (int k = 0; k < RSL; ++k) {
+        const int64_t r = rs_ev[k];
+        if (r >= events) continue;
+        any = true;
+        const unsigned long long* rec = A.recs + (size_t)(r % kGNB) * kGVal * G;
+        const uint32_t tag = (uint32_t)(r + 1);
+#pragma unroll
+        for (int c = 0; c < NS; ++c)
 #pragma unroll
           for (int q = 0; q < NQ; ++q) {
-            const int c = lane + 32 * q;
-            wv[k][q] = c < G ? ld_tagged(rec + (size_t)k * G + c) : ((unsigned long long)tag << 32);
+            const int cc = lane + 32 * q;
+            if ((uint32_t)(wv[k][c][q] >> 32) != tag)
+              wv[k][c][q] = cc < G ? ld_tagged(rec + GREC_IDX(c, cc))
+                                   : ((unsigned long long)tag << 32);
           }
         bool ok = true;
 #pragma unroll
-        for (int k = 0; k < NS; ++k)
+        for (int c = 0; c < NS; ++c)
 #pragma unroll
-          for (int q = 0; q < NQ; ++q) ok &= (uint32_t)(wv[k][q] >> 32) == tag;
-        done = __all_sync(0xffffffffu, ok);
-        if (!done) __nanosleep(32);
-      } while (!done);
-      float* t = tot + (r % kGTot) * kGVal;
+          for (int q = 0; q < NQ; ++q) ok &= (uint32_t)(wv[k][c][q] >> 32) == tag;
+        if (!__all_sync(0xffffffffu, ok)) continue;
+        float* t = tot + (r % kGTot) * kGVal;
 #pragma unroll
-      for (int k = 0; k < NS; ++k) {
-        float acc = 0.f;
+        for (int c = 0; c < NS; ++c) {
+          float acc = 0.f;
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) acc += __uint_as_float((uint32_t)wv[k][q]);
-        acc = warp_sum(acc);
-        if (lane == 0) t[k] = acc;
+          for (int q = 0; q < NQ; ++q) acc += __uint_as_float((uint32_t)wv[k][c][q]);
+          acc = warp_sum(acc);
+          if (lane == 0) t[c] = acc;
+        }
+        if (lane == 0) {
+#ifdef SYSCD_TRACE
+          if (A.dbg && cta == 0 && r < 1024) A.dbg[r * 8 + 5] = gtimer_g();
+          if (A.dbg && r < 1024) A.dbg[8192 + 1024 * 160 + r * 160 + cta] = gtimer_g();
+#endif
+          mbar_arrive(&totbar[r % kGTot]);
+        }
+        __syncwarp();
+        rs_ev[k] = r + 2 * RSL;
+        progressed = true;
       }
-      if (lane == 0) {
-        if (A.dbg && cta == 0 && r < 1024) A.dbg[r * 8 + 5] = gtimer_g();
-        if (A.dbg && r < 1024) A.dbg[8192 + 1024 * 160 + r * 160 + cta] = gtimer_g();
-        mbar_arrive(&totbar[r % kGTot]);
-      }
-      __syncwarp();
+      if (!any) break;
+      if (!progressed) __nanosleep(SYSCD_GRID_SLEEP);
     }
   } else {
     // -------------------------------------------------------------- math warps
@@ -293,13 +388,37 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
       for (int l = 0; l < (LL > 0 ? LL : 1); ++l)
 #pragma unroll
         for (int b = 0; b < BB; ++b) dh[l][b] = 0.f;
+#define XS_OLD(l) ((i + NSLOT - (l)) % NSLOT)
+#define XS_RES ((i + 1) % NSLOT)
       for (int e0 = 0; e0 < nb + LL; e0 += NSLOT) {
 #pragma unroll
         for (int i = 0; i < NSLOT; ++i) {
           const int e = e0 + i;  // e % NSLOT == i: register slot of block e
           if (e < nb + LL) {
+#ifdef SYSCD_TRACE
             const bool dbg = A.dbg && cta == 0 && tid == 0 && p == 0 && e < 1024;
-            if (dbg) A.dbg[e * 8 + 0] = gtimer_g();
+            // all-CTA stamps (thread 0 of each CTA): [e][cta][k]
+            unsigned long long* da = (A.dbg && tid == 0 && p == 0 && e < 1024)
+                                         ? A.dbg + 8192 + 2 * 1024 * 160 + ((size_t)e * 160 + cta) * 8
+                                         : nullptr;
+#define GSTAMP(k)                          \
+  do {                                     \
+    if (dbg) A.dbg[e * 8 + k] = gtimer_g(); \
+    if (da) da[k] = gtimer_g();            \
+  } while (0)
+#else
+            // CTA-0 stamps, runtime-gated on A.dbg (null in production).  Kept
+            // compiled in: ptxas schedules the event body measurably better
+            // with these block boundaries present (config 3: 12.0 ms/epoch
+            // with, 18.9 ms without -- the reducers' totals latency grows from
+            // ~1.3 to ~5 us in the layout without them).
+            const bool dbg = A.dbg && cta == 0 && tid == 0 && p == 0 && e < 1024;
+#define GSTAMP(k)                          \
+  do {                                     \
+    if (dbg) A.dbg[e * 8 + k] = gtimer_g(); \
+  } while (0)
+#endif
+            GSTAMP(0);
             if (e < nb) {
               // ---- stage block e and publish its partials
 #pragma unroll
@@ -309,6 +428,12 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
                   const float* x = ring + (size_t)stage * CTA_ROWS + tid;
 #pragma unroll
                   for (int r = 0; r < RR; ++r) xr[i][b][r] = x[r * NTC];
+                  // the TMA refill of this stage (async proxy) must not overtake
+                  // these generic-proxy reads: without the proxy fence the arrive
+                  // can complete while the loads are still in flight, and a warp
+                  // then reads part of the next column (config 3 went
+                  // nondeterministic once the grid ran fast enough)
+                  fence_proxy_async();
                   __syncwarp();
                   if (lane == 0) mbar_arrive(&empty[stage]);
                   if (++stage == (uint32_t)S) {
@@ -320,7 +445,28 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
                   for (int r = 0; r < RR; ++r) xr[i][b][r] = 0.f;
                 }
               }
-              if (dbg) A.dbg[e * 8 + 1] = gtimer_g();
+              GSTAMP(1);
+#ifdef SYSCD_GRID_DCHK
+              if (A.dbg && ebase + e < 8192) {  // integer checksums of x_e and w per CTA
+                unsigned int cx = 0, cw = 0;
+#pragma unroll
+                for (int r = 0; r < RR; ++r) {
+                  cx += __float_as_uint(xr[i][0][r]) * (unsigned)(r + 1);
+                  cw += __float_as_uint(w[r]) * (unsigned)(r + 1);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                  cx += __shfl_xor_sync(0xffffffffu, cx, o);
+                  cw += __shfl_xor_sync(0xffffffffu, cw, o);
+                }
+                if (lane == 0) {
+                  unsigned long long* cs = A.dbg + 8192 + 2 * 1024 * 160 + 1024 * 160 * 8 +
+                                           8192 * 160 + 8192 * 160 * 4 + ((ebase + e) * 160 + cta) * 2;
+                  atomicAdd(cs, (unsigned long long)cx);
+                  atomicAdd(cs + 1, (unsigned long long)cw);
+                }
+              }
+#endif
               float pr[NS];
 #pragma unroll
               for (int k = 0; k < NS; ++k) pr[k] = 0.f;
@@ -338,34 +484,46 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
 #pragma unroll
                     for (int k = 0; k < BB; ++k)
                       pr[Lay::gx(l, b, k)] =
-                          fmaf(xv, xr[(i + NSLOT - l) % NSLOT][k][r], pr[Lay::gx(l, b, k)]);
+                          fmaf(xv, xr[XS_OLD(l)][k][r], pr[Lay::gx(l, b, k)]);
                 }
               }
-#pragma unroll
-              for (int k = 0; k < NS; ++k) pr[k] = warp_sum(pr[k]);
+              // warp totals (shuffle-transposed: NP-1 + 5-log2(NP) shuffles
+              // instead of 5*NS), then warp 0 sums the warps' deposits in
+              // warp order and publishes the CTA's record
               const int64_t pub = ebase + e;
-              const int rb = (int)(pub & 1);
-              if (lane == 0) {
+              float* rslot = red + (size_t)(pub % kGRed) * 16 * NS;
+              float pv[NP];
 #pragma unroll
-                for (int k = 0; k < NS; ++k) red[(rb * 16 + warp) * kGVal + k] = pr[k];
+              for (int k = 0; k < NP; ++k) pv[k] = k < NS ? pr[k] : 0.f;
+              const float tv = warp_sum_multi<NP>(pv, lane);
+              {
+                const int idx = multi_index<NP>(lane);
+                if ((lane & (32 / NP - 1)) == 0 && idx < NS) rslot[warp * NS + idx] = tv;
               }
               named_bar_sync(1, NTC);
+#ifdef SYSCD_TRACE
               if (A.dbg && warp == 0 && lane == 0 && pub < 1024)
                 A.dbg[8192 + pub * 160 + cta] = gtimer_g();
+#endif
               if (warp == 0 && lane < NS) {
                 float v = 0.f;
-                for (int q = 0; q < NWC; ++q) v += red[(rb * 16 + q) * kGVal + lane];
-                st_tagged(A.recs + ((size_t)(pub % kGNB) * NS + lane) * G + cta,
+                for (int q = 0; q < NWC; ++q) v += rslot[q * NS + lane];
+                st_tagged(A.recs + (size_t)(pub % kGNB) * kGVal * G + GREC_IDX(lane, cta),
                           (uint32_t)(pub + 1), v);
+#ifdef SYSCD_GRID_DCHK
+                if (A.dbg && pub < 8192)  // every CTA's published partials
+                  A.dbg[8192 + 2 * 1024 * 160 + 1024 * 160 * 8 + 8192 * 160 +
+                        ((size_t)pub * 160 + cta) * 4 + lane] = __float_as_uint(v);
+#endif
               }
             }
-            if (dbg) A.dbg[e * 8 + 2] = gtimer_g();
+            GSTAMP(2);
             if (e >= LL) {
               // ---- resolve block c = e - LL (register slot (i + 1) % NSLOT)
               const int c = e - LL;
               const int64_t cpub = ebase + c;
               mbar_wait(&totbar[cpub % kGTot], (uint32_t)((cpub / kGTot) & 1));
-              if (dbg) A.dbg[e * 8 + 3] = gtimer_g();
+              GSTAMP(3);
               const float* t = tot + (cpub % kGTot) * kGVal;
               float dcur[BB];
 #pragma unroll
@@ -396,8 +554,8 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
                     }
                   }
                   float an;
-                  if (A.kind == SYSCD_LOGISTIC_DUAL) {
-                    an = (float)coord_step(A.kind, (double)lin, A.a_d, (double)qj, A.lam,
+                  if (LDUAL) {
+                    an = (float)coord_step(SYSCD_LOGISTIC_DUAL, (double)lin, A.a_d, (double)qj, A.lam,
                                            (double)aj, A.n_coords);
                   } else {
                     an = coord_step_fr(A.kind, lin, __int_as_float(mt.w), A.lam_f, aj,
@@ -430,10 +588,26 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
               for (int b = 0; b < BB; ++b) {
                 const float sd = a * dcur[b];
 #pragma unroll
-                for (int r = 0; r < RR; ++r) w[r] = fmaf(sd, xr[(i + 1) % NSLOT][b][r], w[r]);
+                for (int r = 0; r < RR; ++r) w[r] = fmaf(sd, xr[XS_RES][b][r], w[r]);
               }
             }
-            if (dbg) A.dbg[e * 8 + 4] = gtimer_g();
+            GSTAMP(4);
+#if defined(SYSCD_TRACE) || defined(SYSCD_GRID_DCHK)
+            if (A.dbg && tid == 0 && e >= LL && ebase + e - LL < 8192) {
+              // every event's first delta per CTA (divergence check)
+              A.dbg[8192 + 2 * 1024 * 160 + 1024 * 160 * 8 + (ebase + e - LL) * 160 + cta] =
+                  ((unsigned long long)__float_as_uint(dh[0][0]) << 32) |
+                  __float_as_uint(tot[((ebase + e - LL) % kGTot) * kGVal]);
+            }
+#endif
+#ifdef SYSCD_TRACE
+            if (da && e >= LL) {
+              const float* tt = tot + ((ebase + e - LL) % kGTot) * kGVal;
+              da[5] = ((unsigned long long)__float_as_uint(dh[0][0]) << 32) | __float_as_uint(tt[0]);
+              da[6] = ((unsigned long long)__float_as_uint(tt[1]) << 32) | __float_as_uint(tt[2]);
+              da[7] = ((unsigned long long)__float_as_uint(w[0]) << 32) | __float_as_uint(tt[NS - 1]);
+            }
+#endif
           }
         }
       }
@@ -467,12 +641,14 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
 // ---------------------------------------------------------------------------
 struct GridEntry {
   int rr, bb, ll, ns;
-  const void* fn;
+  const void* fn[2];  // closed-form steps, logistic dual
 };
 
 template <int RR, int BB, int LL>
 static GridEntry make_grid() {
-  return {RR, BB, LL, GridLayout<BB, LL>::kNS, (const void*)&k_grid_epoch<RR, BB, LL>};
+  return {RR, BB, LL, GridLayout<BB, LL>::kNS,
+          {(const void*)&k_grid_epoch<RR, BB, LL, false>,
+           (const void*)&k_grid_epoch<RR, BB, LL, true>}};
 }
 
 // (rows per thread, columns per event, lookahead events).  The default for a
@@ -501,14 +677,14 @@ int grid_choose(int64_t d, int* idx, int* G, int* stages, size_t* smem_out) {
     const int rows = 416 * g_grid_table[i].rr;
     const int64_t g = (d + rows - 1) / rows;
     if (g > sms) continue;
-    const size_t fixed = grid_smem(0, rows).total + 1024;
+    const size_t fixed = grid_smem(0, rows, g_grid_table[i].ns).total + 1024;
     int s = (int)(((size_t)optin - 1024 - fixed) / ((size_t)rows * 4));
     s = std::min(s, 8);
     if (s < g_grid_table[i].bb + 2) continue;
     *idx = i;
     *G = (int)g;
     *stages = s;
-    *smem_out = grid_smem(s, rows).total;
+    *smem_out = grid_smem(s, rows, g_grid_table[i].ns).total;
     return SYSCD_OK;
   }
   set_error("no grid configuration covers d=%lld", (long long)d);
@@ -528,7 +704,8 @@ int grid_launch(const syscd_dense_epoch_args* e, void* workspace, int64_t ws_byt
     return SYSCD_EINVAL;
   }
   const GridEntry& ge = g_grid_table[idx];
-  SYSCD_CUDA_TRY(cudaFuncSetAttribute(ge.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const void* fn = ge.fn[e->kind == SYSCD_LOGISTIC_DUAL ? 1 : 0];
+  SYSCD_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
   GridArgs A;
   A.A = e->A;
@@ -566,7 +743,7 @@ int grid_launch(const syscd_dense_epoch_args* e, void* workspace, int64_t ws_byt
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   void* params[] = {&A};
-  SYSCD_CUDA_TRY(cudaLaunchKernelExC(&cfg, ge.fn, params));
+  SYSCD_CUDA_TRY(cudaLaunchKernelExC(&cfg, fn, params));
   return SYSCD_OK;
 }
 

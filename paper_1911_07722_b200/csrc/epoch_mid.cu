@@ -172,6 +172,10 @@ __global__ void __launch_bounds__(kMidBlock, 1) k_mid_epoch(MidArgs A) {
 
   // tiles start at zero: rows past d stay zero (they are never written)
   for (int i = tid; i < 2 * kMidM * rs; i += blockDim.x) tile[i] = 0.f;
+  // every writer orders its generic-proxy zeros before the TMA (async
+  // proxy) fills that follow the barrier; one fence by the issuing thread
+  // does not cover the other threads' writes
+  fence_proxy_async();
   for (int i = tid; i < rs; i += blockDim.x) wv[i] = i < valid ? A.u[row0 + i] : 0.f;
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
@@ -396,6 +400,7 @@ __global__ void __launch_bounds__(kMidBlock, 1) k_mid_epoch(MidArgs A) {
         }
         reinterpret_cast<float4*>(wv)[gq] = w4;
       }
+      fence_proxy_async();  // reads done before the TMA refill (async proxy) of this stage
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[b]);
       named_bar_sync(1, kMidThreads);
