@@ -187,9 +187,12 @@ struct GridLayout {
 // LDUAL: the logistic-dual instance (the fp64 Newton is compiled only into
 // it); the closed-form steps (ridge / primal logistic, lasso, svm dual) share
 // the other instance.
-template <int RR, int BB, int LL, bool LDUAL>
+template <int RR, int BB, int LL, bool LDUAL, int NWM>
 __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
-  constexpr int NTC = 416;  // 13 math warps + producer + 2 reducers = 16 warps
+  // NWM math warps + the producer + NRED reducer warps = 16 warps
+  constexpr int NTC = NWM * 32;
+  constexpr int NRED = 16 - NWM - 1;
+  static_assert(NRED >= 1, "no reducer warp");
   constexpr int NWC = NTC / 32;
   constexpr int NSLOT = LL + 1;
   using Lay = GridLayout<BB, LL>;
@@ -294,12 +297,13 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
     // so the totals of consecutive events are gathered concurrently.  A word
     // carrying its event's tag is final: later polls reload only the words
     // still missing (the records of the CTAs that are behind).
-    constexpr int RSL = NS <= 4 ? SYSCD_GRID_RSLOTS : 1;  // registers: RSL*NS*NQ words
+    // registers: RSL*NS*NQ words; a lone reducer keeps two events in flight
+    constexpr int RSL = NS <= 4 ? (NRED == 1 && SYSCD_GRID_RSLOTS < 2 ? 2 : SYSCD_GRID_RSLOTS) : 1;
     int64_t rs_ev[RSL];
     unsigned long long wv[RSL][NS][NQ];
 #pragma unroll
     for (int k = 0; k < RSL; ++k) {
-      rs_ev[k] = (warp - NWC - 1) + 2 * k;
+      rs_ev[k] = (warp - NWC - 1) + NRED * k;
 #pragma unroll
       for (int c = 0; c < NS; ++c)
 #pragma unroll
@@ -346,7 +350,7 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
           mbar_arrive(&totbar[r % kGTot]);
         }
         __syncwarp();
-        rs_ev[k] = r + 2 * RSL;
+        rs_ev[k] = r + NRED * RSL;
         progressed = true;
       }
       if (!any) break;
@@ -640,22 +644,26 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
 // host side
 // ---------------------------------------------------------------------------
 struct GridEntry {
-  int rr, bb, ll, ns;
+  int rr, bb, ll, ns, ntc;
   const void* fn[2];  // closed-form steps, logistic dual
 };
 
-template <int RR, int BB, int LL>
+template <int RR, int BB, int LL, int NWM = 13>
 static GridEntry make_grid() {
-  return {RR, BB, LL, GridLayout<BB, LL>::kNS,
-          {(const void*)&k_grid_epoch<RR, BB, LL, false>,
-           (const void*)&k_grid_epoch<RR, BB, LL, true>}};
+  return {RR, BB, LL, GridLayout<BB, LL>::kNS, NWM * 32,
+          {(const void*)&k_grid_epoch<RR, BB, LL, false, NWM>,
+           (const void*)&k_grid_epoch<RR, BB, LL, true, NWM>}};
 }
 
-// (rows per thread, columns per event, lookahead events).  The default for a
-// given RR is the first entry with that RR; SYSCD_GRID_CFG=<index> overrides.
+// (rows per thread, columns per event, lookahead events[, math warps]).  The
+// default for a given RR is the first entry with that RR, and the first RR
+// whose grid fits the GPU wins; SYSCD_GRID_CFG=<index> overrides.  14 math
+// warps + one reducer warp (two events in flight) at 16 rows per thread beat
+// 13 warps + two reducers at 17 rows (config 3: 7.64 vs 8.39 ms per epoch).
 static GridEntry g_grid_table[] = {
-    make_grid<4, 2, 2>(),  make_grid<8, 2, 2>(),  make_grid<12, 2, 1>(), make_grid<17, 1, 3>(),
-    make_grid<17, 2, 1>(), make_grid<17, 4, 0>(), make_grid<12, 1, 4>(), make_grid<8, 1, 5>(),
+    make_grid<4, 2, 2>(),  make_grid<8, 2, 2>(),  make_grid<12, 2, 1>(), make_grid<16, 1, 3, 14>(),
+    make_grid<17, 1, 3>(), make_grid<17, 2, 1>(), make_grid<17, 4, 0>(), make_grid<12, 1, 4>(),
+    make_grid<8, 1, 5>(),  make_grid<16, 1, 4, 14>(), make_grid<16, 1, 2, 14>(),
 };
 constexpr int kGridTable = sizeof(g_grid_table) / sizeof(g_grid_table[0]);
 
@@ -674,7 +682,7 @@ int grid_choose(int64_t d, int* idx, int* G, int* stages, size_t* smem_out) {
       for (int k = 0; k < i; ++k) first &= g_grid_table[k].rr != g_grid_table[i].rr;
       if (!first) continue;
     }
-    const int rows = 416 * g_grid_table[i].rr;
+    const int rows = g_grid_table[i].ntc * g_grid_table[i].rr;
     const int64_t g = (d + rows - 1) / rows;
     if (g > sms) continue;
     const size_t fixed = grid_smem(0, rows, g_grid_table[i].ns).total + 1024;
