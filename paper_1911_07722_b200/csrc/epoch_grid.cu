@@ -191,8 +191,9 @@ template <int RR, int BB, int LL, bool LDUAL, int NWM>
 __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
   // NWM math warps + the producer + NRED reducer warps = 16 warps
   constexpr int NTC = NWM * 32;
-  constexpr int NRED = 16 - NWM - 1;
-  static_assert(NRED >= 1, "no reducer warp");
+  constexpr int NRED = 16 - NWM - 1;  // 0: the producer warp also reduces
+  constexpr int NRW = NRED > 0 ? NRED : 1;
+  static_assert(NRED >= 0, "too many math warps");
   constexpr int NWC = NTC / 32;
   constexpr int NSLOT = LL + 1;
   using Lay = GridLayout<BB, LL>;
@@ -246,8 +247,81 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
   }
   __syncthreads();
 
-  if (warp == NWC) {
-    // ---------------------------------------------------------------- producer
+  // ------------------------------------------------------------ reducer state
+  // Each reducer warp keeps RSL events in flight (reducer w, slot k takes
+  // events r = w + NRW*k (mod NRW*RSL), in order per slot): a slot whose event
+  // is complete sums it and hands it over while the other slots keep polling,
+  // so the totals of consecutive events are gathered concurrently.  A word
+  // carrying its event's tag is final: later polls reload only the words
+  // still missing (the records of the CTAs that are behind).
+  // registers: RSL*NS*NQ words; a lone reducer keeps two events in flight
+  constexpr int NQ = 5;  // ceil(148 / 32) CTAs per lane
+  constexpr int RSL = NS <= 4 ? (NRW == 1 && SYSCD_GRID_RSLOTS < 2 ? 2 : SYSCD_GRID_RSLOTS) : 1;
+  // one poll pass over the slots; returns whether any slot is still open and
+  // sets *prog when an event was handed over
+  auto reduce_pass = [&](int64_t (&rs_ev)[RSL], unsigned long long (&wv)[RSL][NS][NQ],
+                         int64_t events, bool* prog) -> bool {
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < RSL; ++k) {
+      const int64_t r = rs_ev[k];
+      if (r >= events) continue;
+      any = true;
+      const unsigned long long* rec = A.recs + (size_t)(r % kGNB) * kGVal * G;
+      const uint32_t tag = (uint32_t)(r + 1);
+#pragma unroll
+      for (int c = 0; c < NS; ++c)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const int cc = lane + 32 * q;
+          if ((uint32_t)(wv[k][c][q] >> 32) != tag)
+            wv[k][c][q] = cc < G ? ld_tagged(rec + GREC_IDX(c, cc))
+                                 : ((unsigned long long)tag << 32);
+        }
+      bool ok = true;
+#pragma unroll
+      for (int c = 0; c < NS; ++c)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) ok &= (uint32_t)(wv[k][c][q] >> 32) == tag;
+      if (!__all_sync(0xffffffffu, ok)) continue;
+      float* t = tot + (r % kGTot) * kGVal;
+#pragma unroll
+      for (int c = 0; c < NS; ++c) {
+        float acc = 0.f;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) acc += __uint_as_float((uint32_t)wv[k][c][q]);
+        acc = warp_sum(acc);
+        if (lane == 0) t[c] = acc;
+      }
+      if (lane == 0) {
+#ifdef SYSCD_TRACE
+        if (A.dbg && cta == 0 && r < 1024) A.dbg[r * 8 + 5] = gtimer_g();
+        if (A.dbg && r < 1024) A.dbg[8192 + 1024 * 160 + r * 160 + cta] = gtimer_g();
+#endif
+        mbar_arrive(&totbar[r % kGTot]);
+      }
+      __syncwarp();
+      rs_ev[k] = r + NRW * RSL;
+      *prog = true;
+    }
+    return any;
+  };
+
+  if (warp >= NWC) {
+    int64_t events = 0;
+    for (int p = 0; p < A.n_parts; ++p) events += (A.wp[p + 1] - A.wp[p] + BB - 1) / BB;
+    const int rw = NRED > 0 ? warp - NWC - 1 : 0;  // reducer index
+    int64_t rs_ev[RSL];
+    unsigned long long wv[RSL][NS][NQ];
+#pragma unroll
+    for (int k = 0; k < RSL; ++k) {
+      rs_ev[k] = rw + NRW * k;
+#pragma unroll
+      for (int c = 0; c < NS; ++c)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) wv[k][c][q] = 0ull;
+    }
+    // producer state (warp NWC)
     int64_t valid = d - row0;
     valid = valid < 0 ? 0 : (valid > CTA_ROWS ? CTA_ROWS : valid);
     const uint32_t bytes = (uint32_t)(((valid + 3) / 4) * 16);
@@ -257,19 +331,28 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
     // no dependent global load sits between two TMA issues
     int jreg = 0;
     float areg = 0.f, qreg = 0.f;
-    for (int64_t s = s_begin; s < s_end; ++s) {
+    int64_t s = s_begin, loaded = -1;
+    // issue the TMA of column s (lane 0) once its stage is free; with
+    // block == false returns false instead of waiting
+    auto produce = [&](bool block) -> bool {
       const int64_t rel = s - s_begin;
-      if ((rel & 31) == 0) {
+      if ((rel & 31) == 0 && loaded != rel) {
         const int64_t q = s + lane;
         jreg = q < s_end ? A.seq[q] : 0;
         areg = q < s_end ? A.alpha[jreg] : 0.f;
         qreg = q < s_end ? __ldg(A.sq + jreg) : 0.f;
+        loaded = rel;
+      }
+      if (!block) {
+        uint32_t ok = 0;
+        if (lane == 0) ok = mbar_test(&empty[stage], phase ^ 1u) ? 1u : 0u;
+        if (!__shfl_sync(0xffffffffu, ok, 0)) return false;
       }
       const int j = __shfl_sync(0xffffffffu, jreg, (int)(rel & 31));
       const float aj = __shfl_sync(0xffffffffu, areg, (int)(rel & 31));
       const float qj = __shfl_sync(0xffffffffu, qreg, (int)(rel & 31));
       if (lane == 0) {
-        mbar_wait(&empty[stage], phase ^ 1u);
+        if (block) mbar_wait(&empty[stage], phase ^ 1u);
         meta[rel & (kGMeta - 1)] = make_int4(j, __float_as_int(aj), __float_as_int(qj),
                                              __float_as_int(step_inv(A.kind, A.a, qj, A.lam_f)));
         if (bytes) {
@@ -279,82 +362,34 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
         } else {
           mbar_arrive(&full[stage]);
         }
-        if (++stage == (uint32_t)S) {
-          stage = 0;
-          phase ^= 1u;
-        }
       }
+      if (++stage == (uint32_t)S) {
+        stage = 0;
+        phase ^= 1u;
+      }
+      ++s;
       __syncwarp();
-    }
-  } else if (warp > NWC) {
-    // ---------------------------------------------------------------- reducers
-    constexpr int NQ = 5;  // ceil(148 / 32) CTAs per lane
-    int64_t events = 0;
-    for (int p = 0; p < A.n_parts; ++p) events += (A.wp[p + 1] - A.wp[p] + BB - 1) / BB;
-    // Each reducer warp keeps RSL events in flight (warp w, slot k takes
-    // events r = w + 2k (mod 2*RSL), in order per slot): a slot whose event is
-    // complete sums it and hands it over while the other slots keep polling,
-    // so the totals of consecutive events are gathered concurrently.  A word
-    // carrying its event's tag is final: later polls reload only the words
-    // still missing (the records of the CTAs that are behind).
-    // registers: RSL*NS*NQ words; a lone reducer keeps two events in flight
-    constexpr int RSL = NS <= 4 ? (NRED == 1 && SYSCD_GRID_RSLOTS < 2 ? 2 : SYSCD_GRID_RSLOTS) : 1;
-    int64_t rs_ev[RSL];
-    unsigned long long wv[RSL][NS][NQ];
-#pragma unroll
-    for (int k = 0; k < RSL; ++k) {
-      rs_ev[k] = (warp - NWC - 1) + NRED * k;
-#pragma unroll
-      for (int c = 0; c < NS; ++c)
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) wv[k][c][q] = 0ull;
-    }
-    for (;;) {
-      bool any = false, progressed = false;
-#pragma unroll
-      for (int k = 0; k < RSL; ++k) {
-        const int64_t r = rs_ev[k];
-        if (r >= events) continue;
-        any = true;
-        const unsigned long long* rec = A.recs + (size_t)(r % kGNB) * kGVal * G;
-        const uint32_t tag = (uint32_t)(r + 1);
-#pragma unroll
-        for (int c = 0; c < NS; ++c)
-#pragma unroll
-          for (int q = 0; q < NQ; ++q) {
-            const int cc = lane + 32 * q;
-            if ((uint32_t)(wv[k][c][q] >> 32) != tag)
-              wv[k][c][q] = cc < G ? ld_tagged(rec + GREC_IDX(c, cc))
-                                   : ((unsigned long long)tag << 32);
-          }
-        bool ok = true;
-#pragma unroll
-        for (int c = 0; c < NS; ++c)
-#pragma unroll
-          for (int q = 0; q < NQ; ++q) ok &= (uint32_t)(wv[k][c][q] >> 32) == tag;
-        if (!__all_sync(0xffffffffu, ok)) continue;
-        float* t = tot + (r % kGTot) * kGVal;
-#pragma unroll
-        for (int c = 0; c < NS; ++c) {
-          float acc = 0.f;
-#pragma unroll
-          for (int q = 0; q < NQ; ++q) acc += __uint_as_float((uint32_t)wv[k][c][q]);
-          acc = warp_sum(acc);
-          if (lane == 0) t[c] = acc;
-        }
-        if (lane == 0) {
-#ifdef SYSCD_TRACE
-          if (A.dbg && cta == 0 && r < 1024) A.dbg[r * 8 + 5] = gtimer_g();
-          if (A.dbg && r < 1024) A.dbg[8192 + 1024 * 160 + r * 160 + cta] = gtimer_g();
-#endif
-          mbar_arrive(&totbar[r % kGTot]);
-        }
-        __syncwarp();
-        rs_ev[k] = r + NRED * RSL;
-        progressed = true;
+      return true;
+    };
+    if (NRED > 0 && warp == NWC) {
+      // ------------------------------------------------------------ producer
+      while (s < s_end) produce(true);
+    } else if (NRED > 0) {
+      // ------------------------------------------------------------ reducers
+      for (;;) {
+        bool prog = false;
+        if (!reduce_pass(rs_ev, wv, events, &prog)) break;
+        if (!prog) __nanosleep(SYSCD_GRID_SLEEP);
       }
-      if (!any) break;
-      if (!progressed) __nanosleep(SYSCD_GRID_SLEEP);
+    } else {
+      // ------------------------- producer and reducer in one warp (NRED == 0)
+      for (;;) {
+        bool prog = false;
+        while (s < s_end && produce(false)) prog = true;
+        const bool open = reduce_pass(rs_ev, wv, events, &prog);
+        if (!open && s >= s_end) break;
+        if (!prog) __nanosleep(SYSCD_GRID_SLEEP);
+      }
     }
   } else {
     // -------------------------------------------------------------- math warps
@@ -664,6 +699,7 @@ static GridEntry g_grid_table[] = {
     make_grid<4, 2, 2>(),  make_grid<8, 2, 2>(),  make_grid<12, 2, 1>(), make_grid<16, 1, 3, 14>(),
     make_grid<17, 1, 3>(), make_grid<17, 2, 1>(), make_grid<17, 4, 0>(), make_grid<12, 1, 4>(),
     make_grid<8, 1, 5>(),  make_grid<16, 1, 4, 14>(), make_grid<16, 1, 2, 14>(),
+    make_grid<15, 1, 3, 15>(),
 };
 constexpr int kGridTable = sizeof(g_grid_table) / sizeof(g_grid_table[0]);
 
