@@ -244,8 +244,10 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
           for (int c = 0; c < NCH; ++c) {
             mbar_wait(&empty[stage], phase ^ 1u);
             const uint32_t bytes = chunk_bytes[c];
+#if defined(SYSCD_TRACE) || defined(SYSCD_DENSE_STAMPS)
             if (args.dbg != nullptr && blockIdx.x == 0 && s - s_begin < 512)
               args.dbg[7168 + (s - s_begin) * 8 + c] = gtimer();
+#endif
             if (bytes) {
               mbar_arrive_expect_tx(&full[stage], bytes);
               tma_load_1d(ring + (size_t)stage * CHUNK, uslice + c * CHUNK, bytes, &full[stage],
@@ -284,7 +286,11 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
       peer_bar = cluster_map(smem_addr(&xbar[0]), (uint32_t)lane);
     }
     const float* ring_t = ring + tid;
+#if defined(SYSCD_TRACE) || defined(SYSCD_DENSE_STAMPS)
     const bool dbg = args.dbg != nullptr && blockIdx.x == 0 && tid == 0;
+#else
+    constexpr bool dbg = false;  // stamps only in the trace build (scripts/timeline.py)
+#endif
     for (int64_t s = s_begin; s < s_end; ++s) {
       const uint32_t t = (uint32_t)(s - s_begin);
       const uint32_t buf = t & 1u;

@@ -446,15 +446,10 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
     if (da) da[k] = gtimer_g();            \
   } while (0)
 #else
-            // CTA-0 stamps, runtime-gated on A.dbg (null in production).  Kept
-            // compiled in: ptxas schedules the event body measurably better
-            // with these block boundaries present (config 3: 12.0 ms/epoch
-            // with, 18.9 ms without -- the reducers' totals latency grows from
-            // ~1.3 to ~5 us in the layout without them).
-            const bool dbg = A.dbg && cta == 0 && tid == 0 && p == 0 && e < 1024;
-#define GSTAMP(k)                          \
-  do {                                     \
-    if (dbg) A.dbg[e * 8 + k] = gtimer_g(); \
+            // no stamps in production: the runtime-gated CTA-0 stamps cost 13%
+            // of config 3 (7.49 -> 6.53 ms) once the grid stopped convoying
+#define GSTAMP(k) \
+  do {            \
   } while (0)
 #endif
             GSTAMP(0);

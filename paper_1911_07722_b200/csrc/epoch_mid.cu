@@ -257,7 +257,11 @@ __global__ void __launch_bounds__(kMidBlock, 1) k_mid_epoch(MidArgs A) {
     if (s1 == A.wp[p]) continue;
     for (int64_t c0 = A.wp[p]; c0 < s1; c0 += kMidM, ++k) {
       const int b = k & 1;
+#if defined(SYSCD_TRACE) || defined(SYSCD_DENSE_STAMPS)
       const bool dbg = A.dbg && blockIdx.x == 0 && tid == 0 && k < 256;
+#else
+      constexpr bool dbg = false;  // stamps only in the trace build (scripts/timeline_mid.py)
+#endif
       if (dbg) A.dbg[k * 8 + 0] = clock64();
       mbar_wait(&full[b], (k >> 1) & 1);
       if (dbg) A.dbg[k * 8 + 1] = clock64();

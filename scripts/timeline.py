@@ -1,7 +1,10 @@
 """Per-step phase timeline of the dense epoch kernel (CTA 0)."""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ["SYSCD_TRACE"] = "1"  # the stamps exist only in the instrumented build
 import numpy as np, torch
+from paper_1911_07722_b200.csrc.build import build
+build()
 from paper_1911_07722_b200._lib import lib
 from paper_1911_07722_b200.configs import workload
 from paper_1911_07722_b200.device import Dist
