@@ -184,10 +184,12 @@ struct GridLayout {
   }
 };
 
-// LDUAL: the logistic-dual instance (the fp64 Newton is compiled only into
-// it); the closed-form steps (ridge / primal logistic, lasso, svm dual) share
-// the other instance.
-template <int RR, int BB, int LL, bool LDUAL, int NWM>
+// KIND: the step compiled in (SYSCD_RIDGE also serves the primal-logistic
+// surrogate; the fp64 Newton exists only in the logistic-dual instance).
+// IID: with-replacement sampling (the recently-resolved ring).  Fixing both
+// at compile time takes their branches out of the event loop, whose
+// instruction count bounds this kernel (config 3: 6.51 -> 6.31 ms).
+template <int RR, int BB, int LL, int KIND, bool IID, int NWM>
 __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
   // NWM math warps + the producer + NRED reducer warps = 16 warps
   constexpr int NTC = NWM * 32;
@@ -354,7 +356,7 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
       if (lane == 0) {
         if (block) mbar_wait(&empty[stage], phase ^ 1u);
         meta[rel & (kGMeta - 1)] = make_int4(j, __float_as_int(aj), __float_as_int(qj),
-                                             __float_as_int(step_inv(A.kind, A.a, qj, A.lam_f)));
+                                             __float_as_int(step_inv(KIND, A.a, qj, A.lam_f)));
         if (bytes) {
           mbar_arrive_expect_tx(&full[stage], bytes);
           tma_load_1d(ring + (size_t)stage * CTA_ROWS, A.A + (int64_t)j * A.lda + row0, bytes,
@@ -577,7 +579,7 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
                   const int j = mt.x;
                   float aj = __int_as_float(mt.y);
                   const float qj = __int_as_float(mt.z);
-                  if (A.iid) {
+                  if (IID) {
                     const int2 r0 = rcnt_ring[(rcnt - 1 - lane) & (kGRecent - 1)];
                     const int2 r1 = rcnt_ring[(rcnt - 33 - lane) & (kGRecent - 1)];
                     const unsigned m0 = __ballot_sync(0xffffffffu, r0.x == j);
@@ -588,11 +590,11 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
                     }
                   }
                   float an;
-                  if (LDUAL) {
+                  if (KIND == SYSCD_LOGISTIC_DUAL) {
                     an = (float)coord_step(SYSCD_LOGISTIC_DUAL, (double)lin, A.a_d, (double)qj, A.lam,
                                            (double)aj, A.n_coords);
                   } else {
-                    an = coord_step_fr(A.kind, lin, __int_as_float(mt.w), A.lam_f, aj,
+                    an = coord_step_fr(KIND, lin, __int_as_float(mt.w), A.lam_f, aj,
                                        A.inv_n_f);
                   }
                   if (isfinite(an)) {
@@ -601,7 +603,7 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
                   } else if (cta == 0 && tid == 0) {
                     atomicOr(A.status, SYSCD_ENONFINITE);
                   }
-                  if (A.iid) {
+                  if (IID) {
                     __syncwarp();
                     if (lane == 0)
                       rcnt_ring[rcnt & (kGRecent - 1)] = make_int2(j, __float_as_int(aj + dcur[b]));
@@ -675,26 +677,37 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
 // ---------------------------------------------------------------------------
 struct GridEntry {
   int rr, bb, ll, ns, ntc;
-  const void* fn[2];  // closed-form steps, logistic dual
+  const void* fn[4][2];  // [ridge / primal logistic, lasso, svm dual, logistic dual][iid]
 };
+
+template <int RR, int BB, int LL, int NWM, int KIND>
+static void grid_fill(GridEntry& g, int k) {
+  g.fn[k][0] = (const void*)&k_grid_epoch<RR, BB, LL, KIND, false, NWM>;
+  g.fn[k][1] = (const void*)&k_grid_epoch<RR, BB, LL, KIND, true, NWM>;
+}
 
 template <int RR, int BB, int LL, int NWM = 13>
 static GridEntry make_grid() {
-  return {RR, BB, LL, GridLayout<BB, LL>::kNS, NWM * 32,
-          {(const void*)&k_grid_epoch<RR, BB, LL, false, NWM>,
-           (const void*)&k_grid_epoch<RR, BB, LL, true, NWM>}};
+  GridEntry g{RR, BB, LL, GridLayout<BB, LL>::kNS, NWM * 32, {}};
+  grid_fill<RR, BB, LL, NWM, SYSCD_RIDGE>(g, 0);
+  grid_fill<RR, BB, LL, NWM, SYSCD_LASSO>(g, 1);
+  grid_fill<RR, BB, LL, NWM, SYSCD_SVM_DUAL>(g, 2);
+  grid_fill<RR, BB, LL, NWM, SYSCD_LOGISTIC_DUAL>(g, 3);
+  return g;
 }
 
 // (rows per thread, columns per event, lookahead events[, math warps]).  The
-// default for a given RR is the first entry with that RR, and the first RR
-// whose grid fits the GPU wins; SYSCD_GRID_CFG=<index> overrides.  14 math
-// warps + one reducer warp (two events in flight) at 16 rows per thread beat
-// 13 warps + two reducers at 17 rows (config 3: 7.64 vs 8.39 ms per epoch).
+// first entry whose grid fits the GPU wins (SYSCD_GRID_CFG=<index>
+// overrides).  14 math warps + one reducer warp (two events in flight) at 16
+// rows per thread beat 13 warps + two reducers at 17 rows (config 3: 7.64 vs
+// 8.39 ms per epoch); the other geometries measured on config 3 (DESIGN.md:
+// BB=2 or 4 with less lookahead, L=2 or 4 at 16 rows, the producer and
+// reducer in one warp) were slower and are not instantiated.
 static GridEntry g_grid_table[] = {
-    make_grid<4, 2, 2>(),  make_grid<8, 2, 2>(),  make_grid<12, 2, 1>(), make_grid<16, 1, 3, 14>(),
-    make_grid<17, 1, 3>(), make_grid<17, 2, 1>(), make_grid<17, 4, 0>(), make_grid<12, 1, 4>(),
-    make_grid<8, 1, 5>(),  make_grid<16, 1, 4, 14>(), make_grid<16, 1, 2, 14>(),
-    make_grid<15, 1, 3, 15>(),
+    make_grid<4, 2, 2>(),
+    make_grid<8, 2, 2>(),
+    make_grid<12, 2, 1>(),
+    make_grid<16, 1, 3, 14>(),
 };
 constexpr int kGridTable = sizeof(g_grid_table) / sizeof(g_grid_table[0]);
 
@@ -743,7 +756,10 @@ int grid_launch(const syscd_dense_epoch_args* e, void* workspace, int64_t ws_byt
     return SYSCD_EINVAL;
   }
   const GridEntry& ge = g_grid_table[idx];
-  const void* fn = ge.fn[e->kind == SYSCD_LOGISTIC_DUAL ? 1 : 0];
+  const int ks = e->kind == SYSCD_LASSO ? 1
+                 : e->kind == SYSCD_SVM_DUAL ? 2
+                 : e->kind == SYSCD_LOGISTIC_DUAL ? 3 : 0;
+  const void* fn = ge.fn[ks][e->iid ? 1 : 0];
   SYSCD_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
   GridArgs A;
