@@ -76,11 +76,14 @@ __device__ __forceinline__ void rep_store(unsigned long long* dv, int64_t r, uin
   dv[r] = ((unsigned long long)tag << 32) | __float_as_uint(v);
 }
 
+// KIND is the kernel instance's step (SYSCD_RIDGE also serves the primal
+// logistic surrogate): no runtime switch and no fp64 Newton code in the
+// closed-form instances' chain.
+template <int KIND>
 __device__ __forceinline__ float sparse_step(const SparseArgs& A, float lin, float aj, float qj) {
-  if (A.kind == SYSCD_LOGISTIC_DUAL)
-    return (float)coord_step(A.kind, (double)lin, A.a_d, (double)qj, A.lam, (double)aj,
-                             A.n_coords);
-  return coord_step_f(A.kind, lin, A.a, qj, A.lam_f, aj, A.inv_n_f);
+  if (KIND == SYSCD_LOGISTIC_DUAL)
+    return (float)logistic_dual_solve((double)lin, A.a_d * (double)qj, (double)aj, A.n_coords);
+  return coord_step_f(KIND, lin, A.a, qj, A.lam_f, aj, A.inv_n_f);
 }
 
 constexpr int kPcNnz = 512;
@@ -310,6 +313,7 @@ __device__ __forceinline__ void pc_patch(PcBuf& N, int r, float nv, float a) {
   }
 }
 
+template <int KIND>
 __global__ void __launch_bounds__(64) k_sparse_epoch(SparseArgs A, int W) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PcSmem& S = *reinterpret_cast<PcSmem*>(smem_raw);
@@ -425,7 +429,7 @@ __global__ void __launch_bounds__(64) k_sparse_epoch(SparseArgs A, int W) {
         }
         part = warp_sum(part);
         const float aj = *(volatile float*)(A.alpha + jj);
-        const float an = sparse_step(A, part, aj, __ldg(A.sq + jj));
+        const float an = sparse_step<KIND>(A, part, aj, __ldg(A.sq + jj));
         float delta = 0.f;
         if (isfinite(an)) {
           delta = an - aj;
@@ -455,7 +459,7 @@ __global__ void __launch_bounds__(64) k_sparse_epoch(SparseArgs A, int W) {
           const float lin = warp_sum(part);
           const int jt = C.col_j[t];
           const float aj = C.alpha_c[t];
-          const float an = sparse_step(A, lin, aj, C.q_c[t]);
+          const float an = sparse_step<KIND>(A, lin, aj, C.q_c[t]);
           float delta = 0.f;
           if (isfinite(an)) {
             delta = an - aj;
@@ -535,9 +539,12 @@ static int sparse_workers(int32_t n_parts) {
   int dev = 0, sms = 148, per_sm = 4;
   if (cudaGetDevice(&dev) == cudaSuccess) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaFuncSetAttribute(k_sparse_epoch, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    // every instance has the same shape: the logistic-dual one (most registers) decides
+    if (cudaFuncSetAttribute(k_sparse_epoch<SYSCD_LOGISTIC_DUAL>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(PcSmem)) == cudaSuccess)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sparse_epoch, 64, sizeof(PcSmem));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sparse_epoch<SYSCD_LOGISTIC_DUAL>,
+                                                    64, sizeof(PcSmem));
   }
   return std::max(1, std::min((int)n_parts, sms * std::max(per_sm, 1)));
 }
@@ -598,9 +605,13 @@ extern "C" int syscd_sparse_epoch(const syscd_sparse_epoch_args* e, void* stream
   cudaStream_t s = (cudaStream_t)stream;
   SYSCD_CUDA_TRY(cudaMemsetAsync(e->delta_v, 0, e->d * sizeof(float), s));
   const size_t smem = sizeof(PcSmem);
+  void (*fn)(SparseArgs, int) = e->kind == SYSCD_LASSO          ? k_sparse_epoch<SYSCD_LASSO>
+                                : e->kind == SYSCD_SVM_DUAL        ? k_sparse_epoch<SYSCD_SVM_DUAL>
+                                : e->kind == SYSCD_LOGISTIC_DUAL   ? k_sparse_epoch<SYSCD_LOGISTIC_DUAL>
+                                                                   : k_sparse_epoch<SYSCD_RIDGE>;
   SYSCD_CUDA_TRY(
-      cudaFuncSetAttribute(k_sparse_epoch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_sparse_epoch<<<W, 64, smem, s>>>(A, W);
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  fn<<<W, 64, smem, s>>>(A, W);
   SYSCD_CUDA_TRY(cudaGetLastError());
   return SYSCD_OK;
 }
