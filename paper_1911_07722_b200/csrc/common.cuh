@@ -378,6 +378,37 @@ __device__ __forceinline__ int64_t nearest_part_start(const int64_t* wp, int n_p
   return lo;
 }
 
+// The same split on a cost that also charges each partition a fixed amount
+// (its replica flush): cost(p) = 100 wp[p] + fc100 p, with fc100 the flush
+// cost in hundredths of an update.  Still a static function of the plan, so
+// the partition -> worker assignment (and the summation order) is
+// deterministic.
+__device__ __forceinline__ int64_t nearest_cost_start(const int64_t* wp, int n_parts, int fc100,
+                                                      int64_t t) {
+  auto cost = [&](int i) { return 100 * wp[i] + (int64_t)fc100 * i; };
+  int lo = 0, hi = n_parts + 1;  // first index with cost >= t
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (cost(mid) < t) {
+      lo = mid + 1;
+    } else {
+      hi = mid;
+    }
+  }
+  if (lo > n_parts) lo = n_parts;
+  if (lo > 0 && t - cost(lo - 1) < cost(lo) - t) --lo;
+  return lo;
+}
+
+__device__ __forceinline__ void worker_parts_cost(const int64_t* wp, int n_parts, int G, int g,
+                                                  int fc100, int64_t* p_lo, int64_t* p_hi) {
+  const int64_t total = 100 * wp[n_parts] + (int64_t)fc100 * n_parts;
+  *p_lo = g == 0 ? 0 : nearest_cost_start(wp, n_parts, fc100, (int64_t)((__int128)total * g / G));
+  *p_hi = g == G - 1 ? n_parts
+                     : nearest_cost_start(wp, n_parts, fc100,
+                                          (int64_t)((__int128)total * (g + 1) / G));
+}
+
 __device__ __forceinline__ void worker_parts(const int64_t* wp, int n_parts, int G, int g,
                                              int64_t* p_lo, int64_t* p_hi) {
   const int64_t total = wp[n_parts];

@@ -67,7 +67,15 @@ constexpr int kMetaRing = 64;
 
 // debug timeline stamp: the SM cycle counter (CTA 0 only, so one clock)
 __device__ __forceinline__ unsigned long long gtimer() { return (unsigned long long)clock64(); }
+__device__ __forceinline__ unsigned long long gtimer_ns() {  // comparable across SMs
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 constexpr int kMaxCluster = 16;
+#ifndef SYSCD_DENSE_FLUSH_COST
+#define SYSCD_DENSE_FLUSH_COST 115  // flush cost in hundredths of a column step
+#endif
 
 template <int NTC, int RC, int NCH>
 struct DenseCfg {
@@ -147,6 +155,9 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
   const int64_t row0 = (int64_t)rank * CTA_ROWS;
   const int64_t d = args.d;
 
+#ifdef SYSCD_TRACE
+  if (args.dbg && tid == 0) args.dbg[12288 + blockIdx.x * 4 + 0] = gtimer_ns();
+#endif
   for (int i = tid; i < S * CHUNK; i += blockDim.x) ring[i] = 0.f;
   for (int i = tid; i < 2 * kMaxCluster; i += blockDim.x) slots[i] = 0.f;
   // every writer orders its generic-proxy zeros before the TMA (async
@@ -161,7 +172,10 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
     mbar_init(&xbar[0], 1);
     mbar_init(&xbar[1], 1);
     int64_t p_lo, p_hi;
-    worker_parts(args.wp, args.n_parts, G, g, &p_lo, &p_hi);
+    // a partition's replica flush costs about 1.15 column steps (config 2:
+    // 2.3 us against 2.0 us per column); balancing columns alone left the
+    // cluster holding the 8-column partitions 7% behind the others
+    worker_parts_cost(args.wp, args.n_parts, G, g, SYSCD_DENSE_FLUSH_COST, &p_lo, &p_hi);
     if (p_lo > args.n_parts) p_lo = args.n_parts;
     if (p_hi > args.n_parts) p_hi = args.n_parts;
     range[0] = p_lo;
@@ -437,7 +451,19 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
     }
   }
   __syncwarp();
+#ifdef SYSCD_TRACE
+  if (args.dbg && tid == 0) {
+    args.dbg[12288 + blockIdx.x * 4 + 1] = gtimer_ns();
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    args.dbg[12288 + blockIdx.x * 4 + 3] =
+        ((unsigned long long)smid << 32) | (unsigned long long)(args.wp[range[1]] - args.wp[range[0]]);
+  }
+#endif
   cluster_sync_all();
+#ifdef SYSCD_TRACE
+  if (args.dbg && tid == 0) args.dbg[12288 + blockIdx.x * 4 + 2] = gtimer_ns();
+#endif
 }
 
 // ---------------------------------------------------------------------------

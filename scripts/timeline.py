@@ -15,7 +15,7 @@ wl = workload(cfg_id)
 eng = _Engine(wl.problem, wl.solver, Dist())
 for t in range(3):
     eng.global_round(t)
-buf = torch.zeros(512 * 22, dtype=torch.int64, device="cuda")
+buf = torch.zeros(16384, dtype=torch.int64, device="cuda")
 L = lib(); L.syscd_debug_set_timeline.argtypes = [ctypes.c_void_p]
 L.syscd_debug_set_timeline(buf.data_ptr())
 eng.global_round(3)
@@ -24,7 +24,7 @@ L.syscd_debug_set_timeline(None)
 raw = buf.cpu().numpy().astype(np.float64)
 t = raw[:3072].reshape(512, 6)
 fl = raw[3072:7168].reshape(512, 8)
-pu = raw[7168:].reshape(512, 8)
+pu = raw[7168:7168 + 4096].reshape(512, 8)
 t = t[t[:, 0] > 0] / 1.965  # SM cycles -> ns at the 1965 MHz boost clock
 d = np.diff(t, axis=1)
 step = np.diff(t[:, 0])
@@ -42,3 +42,17 @@ if len(fi):
     print(f"  flush done at +{((fl[fi, 7] - base) / 1.965).mean():.0f} ns ({len(fi)} flushes)")
     for c in range(6):
         print(f"  u chunk {c} wait begins at +{((pu[fi, c] - base) / 1.965).mean():.0f} ns")
+
+# per-CTA kernel spans (trace build): entry, work done, after the final cluster sync, columns
+sp = buf.cpu().numpy()[12288:12288 + 4 * 160].reshape(160, 4).astype(np.float64)
+sp = sp[sp[:, 0] > 0]
+t0 = sp[:, 0].min()
+print(f"CTAs {len(sp)}: entry spread {sp[:,0].max()-t0:.0f} ns; work end min/median/max "
+      f"{sp[:,1].min()-t0:.0f}/{np.median(sp[:,1])-t0:.0f}/{sp[:,1].max()-t0:.0f} ns; exit max {sp[:,2].max()-t0:.0f}")
+cols = sp[:, 3].astype(np.int64) & 0xffffffff
+smid = sp[:, 3].astype(np.int64) >> 32
+C = 16
+for g in range(len(sp) // C):
+    blk = slice(g * C, (g + 1) * C)
+    print(f"  cluster {g}: {int(cols[g * C])} columns, work end {sp[blk, 1].max() - t0:.0f} ns "
+          f"({(sp[blk, 1].max() - t0) / cols[g * C]:.0f} ns/column), SMs {sorted(int(x) for x in smid[blk])[:3]}..{int(smid[blk].max())}")
