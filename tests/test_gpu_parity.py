@@ -273,6 +273,10 @@ def _edge_pair(kind, d, n, seed, zero_cols=(), lam=None):
     (600, 50, dict(K=1, P=5, bucket_size=3, sampling="iid", T3=2, T4=4)),
     (30011, 48, dict(K=1, P=4, bucket_size=4)),     # cluster kernel, ragged last CTA
     (52003, 37, dict(K=1, P=5, bucket_size=3, sampling="iid", T3=2, T4=5)),
+    # one partition of tall columns: the grid-wide kernel (one instance per
+    # step kind and sampling mode), ragged last CTA
+    (60013, 24, dict(K=1, P=1, bucket_size=4)),
+    (60013, 24, dict(K=1, P=1, bucket_size=4, sampling="iid", T3=3, T4=5)),
 ])
 def test_edge_geometries(cuda, kind, d, n, kw):
     from paper_1911_07722_b200 import SolverConfig, run_syscd
