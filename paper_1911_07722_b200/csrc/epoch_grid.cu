@@ -193,9 +193,9 @@ template <int RR, int BB, int LL, int KIND, bool IID, int NWM>
 __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
   // NWM math warps + the producer + NRED reducer warps = 16 warps
   constexpr int NTC = NWM * 32;
-  constexpr int NRED = 16 - NWM - 1;  // 0: the producer warp also reduces
-  constexpr int NRW = NRED > 0 ? NRED : 1;
-  static_assert(NRED >= 0, "too many math warps");
+  constexpr int NRED = 16 - NWM - 1;
+  constexpr int NRW = NRED;
+  static_assert(NRED >= 1, "no reducer warp");
   constexpr int NWC = NTC / 32;
   constexpr int NSLOT = LL + 1;
   using Lay = GridLayout<BB, LL>;
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
   if (warp >= NWC) {
     int64_t events = 0;
     for (int p = 0; p < A.n_parts; ++p) events += (A.wp[p + 1] - A.wp[p] + BB - 1) / BB;
-    const int rw = NRED > 0 ? warp - NWC - 1 : 0;  // reducer index
+    const int rw = warp - NWC - 1;  // reducer index (producer: unused)
     int64_t rs_ev[RSL];
     unsigned long long wv[RSL][NS][NQ];
 #pragma unroll
@@ -334,9 +334,8 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
     int jreg = 0;
     float areg = 0.f, qreg = 0.f;
     int64_t s = s_begin, loaded = -1;
-    // issue the TMA of column s (lane 0) once its stage is free; with
-    // block == false returns false instead of waiting
-    auto produce = [&](bool block) -> bool {
+    // issue the TMA of column s (lane 0) once its stage is free
+    auto produce = [&]() {
       const int64_t rel = s - s_begin;
       if ((rel & 31) == 0 && loaded != rel) {
         const int64_t q = s + lane;
@@ -345,16 +344,11 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
         qreg = q < s_end ? __ldg(A.sq + jreg) : 0.f;
         loaded = rel;
       }
-      if (!block) {
-        uint32_t ok = 0;
-        if (lane == 0) ok = mbar_test(&empty[stage], phase ^ 1u) ? 1u : 0u;
-        if (!__shfl_sync(0xffffffffu, ok, 0)) return false;
-      }
       const int j = __shfl_sync(0xffffffffu, jreg, (int)(rel & 31));
       const float aj = __shfl_sync(0xffffffffu, areg, (int)(rel & 31));
       const float qj = __shfl_sync(0xffffffffu, qreg, (int)(rel & 31));
       if (lane == 0) {
-        if (block) mbar_wait(&empty[stage], phase ^ 1u);
+        mbar_wait(&empty[stage], phase ^ 1u);
         meta[rel & (kGMeta - 1)] = make_int4(j, __float_as_int(aj), __float_as_int(qj),
                                              __float_as_int(step_inv(KIND, A.a, qj, A.lam_f)));
         if (bytes) {
@@ -371,25 +365,15 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
       }
       ++s;
       __syncwarp();
-      return true;
     };
-    if (NRED > 0 && warp == NWC) {
+    if (warp == NWC) {
       // ------------------------------------------------------------ producer
-      while (s < s_end) produce(true);
-    } else if (NRED > 0) {
+      while (s < s_end) produce();
+    } else {
       // ------------------------------------------------------------ reducers
       for (;;) {
         bool prog = false;
         if (!reduce_pass(rs_ev, wv, events, &prog)) break;
-        if (!prog) __nanosleep(SYSCD_GRID_SLEEP);
-      }
-    } else {
-      // ------------------------- producer and reducer in one warp (NRED == 0)
-      for (;;) {
-        bool prog = false;
-        while (s < s_end && produce(false)) prog = true;
-        const bool open = reduce_pass(rs_ev, wv, events, &prog);
-        if (!open && s >= s_end) break;
         if (!prog) __nanosleep(SYSCD_GRID_SLEEP);
       }
     }
