@@ -99,12 +99,21 @@ def surrogate_step(kind, lin, a, q, lam, alpha_j, n_coords):
     return logistic_dual_newton(lin, aq, alpha_j, n_coords) - alpha_j
 
 
-def logistic_dual_newton(lin, aq, alpha_j, n_coords, max_iter=100):
+def _sigmoid(s):
+    return 1.0 / (1.0 + math.exp(-s)) if s >= 0 else math.exp(s) / (1.0 + math.exp(s))
+
+
+def logistic_dual_newton(lin, aq, alpha_j, n_coords, max_iter=200):
     """Root of h(s) = lin + aq (sigma(s) - alpha_j) + s/n over s = logit(t).
 
-    h is strictly increasing (h' = aq s(1-s) + 1/n), so a bracketed Newton
-    with bisection fallback (the safeguarding pattern of objective.py:146-184)
-    converges; working in log-odds keeps t = sigma(s) strictly inside (0, 1).
+    h is strictly increasing (h' = aq s(1-s) + 1/n) with h(lo) < 0 < h(hi)
+    on the bracket below, so a bracketed Newton converges; working in
+    log-odds keeps t = sigma(s) strictly inside (0, 1).  Safeguards (the
+    bracket-and-bisect pattern of objective.py:146-184, tightened): bisect
+    whenever the Newton iterate would leave the bracket or the step is not
+    at least halving (the log-odds Newton oscillates between the sigmoid's
+    flat tails otherwise); stop on a relative step below 1e-13 or when no
+    representable progress is left.
     """
     inv_n = 1.0 / n_coords
     lo = -n_coords * (lin + aq * (1.0 - alpha_j)) - 1.0
@@ -114,8 +123,9 @@ def logistic_dual_newton(lin, aq, alpha_j, n_coords, max_iter=100):
         s = min(max(s, lo), hi)
     else:
         s = min(max(0.0, lo), hi)
+    dx_old = dx = hi - lo
     for _ in range(max_iter):
-        t = 1.0 / (1.0 + math.exp(-s)) if s >= 0 else math.exp(s) / (1.0 + math.exp(s))
+        t = _sigmoid(s)
         h = lin + aq * (t - alpha_j) + s * inv_n
         if h > 0.0:
             hi = s
@@ -124,14 +134,18 @@ def logistic_dual_newton(lin, aq, alpha_j, n_coords, max_iter=100):
         else:
             break
         dh = aq * t * (1.0 - t) + inv_n
-        ns = s - h / dh
-        if not (lo < ns < hi):
-            ns = 0.5 * (lo + hi)
-        step = ns - s
-        s = ns
-        if abs(step) <= 1e-13 * max(1.0, abs(s)):
+        if ((s - hi) * dh - h) * ((s - lo) * dh - h) > 0.0 or abs(2.0 * h) > abs(dx_old * dh):
+            dx_old, dx = dx, 0.5 * (hi - lo)
+            ns = lo + dx
+        else:
+            dx_old, dx = dx, h / dh
+            ns = s - dx
+        if ns == s:
             break
-    return 1.0 / (1.0 + math.exp(-s)) if s >= 0 else math.exp(s) / (1.0 + math.exp(s))
+        s = ns
+        if abs(dx) <= 1e-13 * max(1.0, abs(s)):
+            break
+    return _sigmoid(s)
 
 
 def duality_gap(kind, alpha, v, atw_fn, y, lam, n_coords):

@@ -293,7 +293,11 @@ class _Engine:
         if nxt.lo is not None and nxt.lo <= rid < nxt.hi:
             main.wait_event(nxt.ready)
         else:
+            # re-plan into nxt: its last consumer (free) AND its last writer
+            # (ready: recorded after every plan, also the side-stream
+            # prefetch queued after free was recorded) must be done
             main.wait_event(nxt.free)
+            main.wait_event(nxt.ready)
             self._plan(nxt, rid, main)
         cur.free.record(main)
         self.cur = 1 - self.cur
@@ -410,14 +414,18 @@ class _Engine:
                                            dp.lam, dp.n_coords, self._p_u, _stream()),
                   "syscd_apply_dv")
             return
-        # T2 > 1: node-local rounds with the drift term (solvers.py:373-398)
+        # T2 > 1: node-local rounds with the drift term (solvers.py:373-398).
+        # Nodes are independent within a global round, so the node loop is the
+        # inner one: round ids are consumed in increasing order (the plan
+        # tables are prefetched in that order) with one v_node per local node.
         drift = cfg.K * dp.gamma
         delta_sum = torch.zeros(dp.d, dtype=torch.float64, device="cuda")
         u_k = torch.zeros_like(self._u_buf)[:dp.d]
-        for k in range(self.K_local):
-            v_node = self.v.clone()
-            for t2 in range(cfg.T2):
-                rid = t1 * cfg.T2 + t2
+        v_nodes = [self.v.clone() for _ in range(self.K_local)]
+        for t2 in range(cfg.T2):
+            rid = t1 * cfg.T2 + t2
+            for k in range(self.K_local):
+                v_node = v_nodes[k]
                 if t2 == 0:
                     u_k.copy_(self.u)
                 else:
@@ -425,6 +433,7 @@ class _Engine:
                 self.epoch(rid, u_k, k, k + 1)
                 call("syscd_apply_dv", dp.kind, dp.d, _ptr(self.dv), _ptr(v_node), None, dp.lam,
                      dp.n_coords, None, _stream())
+        for v_node in v_nodes:  # ascending node order (reduce_replicas, solvers.py:423)
             delta_sum += v_node - self.v
         self.dist.allreduce_(delta_sum)
         self.v += delta_sum
