@@ -2,21 +2,26 @@
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
 
-A step is one global round (= one epoch with the default T3/T4) of the
-configured workload with A resident in HBM: device planning of the round's
-permutations, the epoch kernel over all partitions, the replica reduction,
-[N>1: NCCL all-reduce of dv], and the v/grad epilogue.  Metrics (a fresh A
-alpha) are outside the timed region, as in the reference (solvers.py:425).
+Default workload: BASELINE config 3 (ridge 1M x 8000, 32 GB fp32), the
+largest single-GPU configuration and the one BASELINE scales over 1/2/4/8
+GPUs.  A step is one global round (= one epoch with the default T3/T4) with
+A resident in HBM: device planning of the round's permutations, the epoch
+kernel over all partitions, the replica reduction, [N>1: NCCL all-reduce of
+dv], and the v/grad epilogue.  Metrics (a fresh A alpha) are outside the timed
+region, as in the reference (solvers.py:425).
 
 value      = coordinate updates/s of the whole job (sum over ranks / max time)
 roofline   = the epoch kernel's algorithmic A-stream bytes / its CUDA-event
              duration vs the measured HBM copy bandwidth (MEASURED_PEAKS.json)
-e2e        = the same metric through the public API run_syscd() on a
-             host-resident problem: every step uploads A and y from pinned
+e2e        = the same metric through the public API run_syscd() on host data:
+             every step uploads this rank's shard (A and y) from pinned
              memory, runs the configured epochs and reads alpha back
-cpu_baseline = the oracle's chain timed on the host cores (oracle/cpu_baseline)
+cpu_baseline = the C++/OpenMP fp64 oracle (oracle/syscd_cpu.cpp) on the same
+             problem, same K/P/B/seed, a bounded number of rounds
+--impl reference: the same oracle on the same workload as the reference arm
+             (rank 0 only), one round per step, all host cores.
 Extra keys: a_stream_gbs, epochs_per_s, time_to_target (relative
-suboptimality 1e-4 against F* from a K=P=1 GPU solve).
+suboptimality 1e-4 against F*).
 """
 
 from __future__ import annotations
@@ -31,7 +36,10 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CONFIG_DEFAULT = 2
+CONFIG_DEFAULT = 3
+# BASELINE.json's metric, printed verbatim by both arms (the driver divides them)
+METRIC = "coord updates/s and A-stream GB/s per epoch; time to 1e-4 rel. suboptimality"
+DTYPE = "f32 (A, replicas, dots, closed-form steps; fp64 v, logistic-dual polish, metrics)"
 
 
 def parse():
@@ -45,7 +53,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-ttt", action="store_true")
-    p.add_argument("--cpu-budget", type=float, default=8.0)
+    p.add_argument("--cpu-budget", type=float, default=20.0)
     return p.parse_args()
 
 
@@ -127,39 +135,47 @@ def dist_setup(n_gpus):
     return world, rank, local
 
 
-def f_star_for(problem, cfg_id, epochs=200):
-    """High-accuracy optimum for relative suboptimality: the same problem
-    solved with K=P=1 (exact updates, a = gamma) until the relative model
-    change stalls; returns (F*, gap at F*)."""
-    from paper_1911_07722_b200 import SolverConfig, compute_reference_optimum, run_syscd
+def f_star_for(problem, solver, epochs=200, dist=None):
+    """High-accuracy optimum for relative suboptimality; returns (F*,
+    certificate dict).  Ridge: conjugate gradients on the normal equations
+    (cli.py:85-101), certified by the relative residual of (A^T A + lam I)
+    alpha = A^T y (the duality gap of an fp32-rounded alpha is useless at
+    lam = 1e-4: the 1/lam factor amplifies the rounding).  Otherwise the same
+    problem solved with K=P=1 (exact updates, a = gamma) until the relative
+    model change stalls, certified by its duality gap."""
+    from paper_1911_07722_b200 import SolverConfig, run_syscd
     from paper_1911_07722_b200.device import Dist
     from paper_1911_07722_b200.objective import RIDGE
-    if problem.kind == RIDGE:  # conjugate gradients on the normal equations (cli.py:85-101)
-        a_star, f_star = compute_reference_optimum(problem)
-        return f_star, problem.device().gap_host(a_star)[0]
-    B = 8
-    cfg = SolverConfig(K=1, P=1, bucket_size=B, T1=None, max_epochs=epochs, tolerance=1e-7,
-                       metrics_every=10_000, compute_gap=True, seed=1)
-    res = run_syscd(problem, cfg, dist=Dist.single())  # the full problem on this rank
+    from paper_1911_07722_b200.optimum import _ridge_cg
+    if problem.kind == RIDGE:
+        x, iters, rel_res = _ridge_cg(problem)
+        f_star = problem.device().objective(x.float())
+        return f_star, {"kind": "CG normal-equation relative residual", "value": rel_res,
+                        "iterations": iters}
+    import dataclasses
+    # one partition per node group; the workload's K, B and seed keep each
+    # rank's shard (the static node partition) unchanged
+    cfg = dataclasses.replace(solver, P=1, T1=None, max_epochs=epochs, tolerance=1e-7,
+                              metrics_every=10_000, compute_gap=True)
+    res = run_syscd(problem, cfg, dist=dist or Dist.single())
     last = res.metrics[-1]
-    return last.objective, last.gap
+    return last.objective, {"kind": "duality gap of a K=P=1 solve", "value": last.gap}
 
 
 def run_ours(args):
     import torch
-    from paper_1911_07722_b200 import run_syscd
     from paper_1911_07722_b200.configs import workload
     from paper_1911_07722_b200.device import Dist
     from paper_1911_07722_b200.solvers import _Engine
 
     world, rank, local = dist_setup(args.gpus)
     dist = Dist()
-    wl = workload(args.config, scale=args.scale, n_gpus=world)
+    # N > 1: every rank generates only its own shard's columns
+    wl = workload(args.config, scale=args.scale, n_gpus=world, dist=dist)
     pb, cfg = wl.problem, wl.solver
     cfg.plan_batch = 8
     eng = _Engine(pb, cfg, dist)
     dp = eng.dp
-    n_local_updates = None
     # warm-up
     for t in range(args.warmup):
         eng.global_round(t)
@@ -209,8 +225,9 @@ def run_ours(args):
     k_avg = sum(kms) / len(kms)
     hbm, peak_kind = peaks()
     achieved = local_a_bytes / (k_avg / 1e3) / 1e9
+    traffic = ncu_traffic(args.config, world) or {}
     out = {
-        "metric": "coord updates/s (A-stream GB/s, time to 1e-4 rel. suboptimality reported beside)",
+        "metric": METRIC,
         "value": value,
         "unit": "updates/s",
         "n_gpus": world,
@@ -218,16 +235,19 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": ms_per_step,
         "higher_is_better": True,
-        "scaling": "strong",  # a fixed problem split over the GPUs (K = N node groups)
+        # per-GPU work is fixed only for config 3 (K = N, P = 1 per GPU: each
+        # GPU streams its own 32/N GB); the others split a fixed problem
+        "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "f32 (fp64 step and metrics)",
-        "data": "synthetic (seeded, BASELINE.json config distributions, generated in HBM)",
+        "dtype": DTYPE,
+        "data": "synthetic (seeded counter-based generator, BASELINE.json config distributions, "
+                "each rank's shard generated in HBM)",
         "config": {
             "workload": f"config{args.config}: {wl.name}",
             "objective": ["ridge", "logistic", "lasso", "svm_dual", "logistic_dual"][pb.kind],
             "d": wl.info["d"], "n": wl.info["n"], "lam": wl.info["lam"],
             "K": cfg.K, "P": cfg.P, "bucket_size": cfg.resolved_bucket_size(),
-            "repartition": cfg.repartition, "epochs_per_step": 1,
+            "repartition": cfg.repartition, "seed": cfg.seed, "epochs_per_step": 1,
             "l2": ("A (%.1f GB) > 126 MB L2: every step streams A from HBM" % (wl.a_bytes / 1e9)
                    if wl.a_bytes > 126e6 else
                    "A fits in L2 (no flush between steps: the solver reuses it every epoch)"),
@@ -244,9 +264,9 @@ def run_ours(args):
             "peak_source": peak_kind,
             "unit": "GB/s",
             "frac": achieved / hbm,
-            "traffic": (ncu_traffic(args.config, world) or {}).get("bytes"),
+            "traffic": traffic.get("bytes"),
             "traffic_unit": "bytes per launch (dram read + write, ncu --set full)",
-            "traffic_source": (ncu_traffic(args.config, world) or {}).get("source"),
+            "traffic_source": traffic.get("source"),
             "kernel_ms": k_avg,
             "kernel_share_of_step": k_avg / ms_per_step,
             "algorithmic_bytes_per_launch": local_a_bytes,
@@ -254,12 +274,16 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clk,
     }
+    del eng
+    host = None
+    if not args.no_e2e or (not args.no_cpu and world == 1):
+        host = host_copy(wl)  # pinned copy of this rank's shard (setup, untimed)
     if not args.no_e2e:  # before the long solves, on a quiet allocator
-        out["e2e"] = e2e_run(args, wl, world, dist)
+        out["e2e"] = e2e_run(wl, host, world, dist)
     if not args.no_ttt:  # every rank takes part (the solve all-reduces dv)
         out["time_to_target"] = time_to_target(wl, args, dist if world > 1 else None)
     if not args.no_cpu and rank == 0 and world == 1:
-        out["cpu_baseline"] = cpu_baseline(wl, eng, args)
+        out["cpu_baseline"] = cpu_baseline(wl, host, args, args.cpu_budget)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -305,15 +329,16 @@ def _epoch_kernel_name(dp, eng):
     return "k_dense_epoch"
 
 
-def dual_suboptimality(pb, res, k, target, epochs=150):
+def dual_suboptimality(pb, solver, res, k, target, epochs=150, dist=None):
     """(D - D*)/(D0 - D*) along a dual run, with D* from a K=P=1 solve (exact
     coordinate updates) certified by its duality gap; reported
     only when the certificate is tighter than the target."""
     from paper_1911_07722_b200 import SolverConfig, run_syscd
     from paper_1911_07722_b200.device import Dist
-    cfg = SolverConfig(K=1, P=1, bucket_size=8, T1=None, max_epochs=epochs, tolerance=1e-8,
-                       metrics_every=10_000, compute_gap=True, seed=1)
-    ref = run_syscd(pb, cfg, dist=Dist.single())
+    import dataclasses
+    cfg = dataclasses.replace(solver, P=1, T1=None, max_epochs=epochs, tolerance=1e-8,
+                              metrics_every=10_000, compute_gap=True)
+    ref = run_syscd(pb, cfg, dist=dist or Dist.single())
     d_star, gap_star = ref.metrics[-1].objective, ref.metrics[-1].gap
     d0 = res.metrics[0].objective
     scale = max(d0 - d_star, 1e-300)
@@ -372,9 +397,9 @@ def time_to_target(wl, args, dist=None, target=1e-4, max_epochs=2000):
                                                  if m.epoch >= wl.solver.T1), None),
                "config_epochs": wl.solver.T1}
         if pb.n_coordinates <= 4_000_000:
-            out["suboptimality"] = dual_suboptimality(pb, res, k, target)
+            out["suboptimality"] = dual_suboptimality(pb, wl.solver, res, k, target, dist=dist)
         return out
-    f_star, gap_star = f_star_for(pb, wl.cfg_id)
+    f_star, cert = f_star_for(pb, wl.solver, dist=dist)
     cfg = dataclasses.replace(wl.solver, T1=max_epochs if wl.cfg_id != 3 else 200,
                               metrics_every=1, compute_gap=False)
     res = run_syscd(pb, cfg, f_star=f_star, dist=dist)
@@ -392,35 +417,37 @@ def time_to_target(wl, args, dist=None, target=1e-4, max_epochs=2000):
     rel_nominal = (res.metrics[min(nominal, len(res.metrics) - 1)].objective - f_star) / (f0 - f_star)
     return {"target": target,
             "definition": "(F-F*)/(F0-F*), F* by GPU CG (ridge) or a K=P=1 GPU solve (lasso)",
-            "f_star": f_star, "f_star_gap": gap_star, "hit": hit,
+            "f_star": f_star, "f_star_certificate": cert, "hit": hit,
             "rel_subopt_at_config_epochs": rel_nominal, "config_epochs": nominal,
             "best_rel_subopt": best, "epochs_run": len(res.metrics) - 1,
             "epoch_seconds_total": t}
 
 
-def e2e_run(args, wl, world, dist):
-    """Public API on host data: pinned upload + run_syscd + alpha download."""
-    import dataclasses
+def host_copy(wl):
+    """This rank's problem data in pinned host memory: the dense store or the
+    CSC arrays, plus y (primal) or the labels (dual)."""
     import torch
-    from paper_1911_07722_b200 import (ColumnMatrix, GlmProblem, LabeledDataset,
-                                       run_syscd)
     pb = wl.problem
     m = pb.data.matrix
-    if m.storage_kind == "dense":
-        if m._dev_dense is None:
-            return None
-        hosts = [torch.empty(m._dev_dense.shape, dtype=torch.float32, pin_memory=True)]
-        hosts[0].copy_(m._dev_dense)
-    else:
-        if m._dev_csc is None:
-            return None
-        hosts = []
-        for t in m._dev_csc:
-            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-            h.copy_(t)
-            hosts.append(h)
-    labels = pb.data.labels.copy()
+    devs = [m._dev_dense] if m.storage_kind == "dense" else list(m._dev_csc)
+    pinned = []
+    for t in devs:
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t)
+        pinned.append(h)
+    return {"tensors": pinned, "labels": pb.data.labels.copy(), "dense": m.storage_kind == "dense",
+            "d": m.n_rows, "n": pb.n_coordinates, "global_cols": m.global_cols}
+
+
+def e2e_run(wl, host, world, dist):
+    """Public API on host data: pinned upload of this rank's shard +
+    GlmProblem.build + run_syscd + alpha download."""
+    import dataclasses
+    import torch
+    from paper_1911_07722_b200 import ColumnMatrix, GlmProblem, LabeledDataset, run_syscd
+    pb = wl.problem
     cfg = dataclasses.replace(wl.solver, metrics_every=10_000_000)
+    labels = host["labels"]
     steps = 3
     times, upd = [], 0
     for s in range(steps + 1):
@@ -428,9 +455,11 @@ def e2e_run(args, wl, world, dist):
         if world > 1:
             torch.distributed.barrier()
         t0 = time.perf_counter()
-        devs = [h.to("cuda", non_blocking=True) for h in hosts]
-        mm = (ColumnMatrix.from_device(devs[0], m.n_rows) if m.storage_kind == "dense" else
-              ColumnMatrix.from_device_csc(*devs, m.n_rows))
+        devs = [h.to("cuda", non_blocking=True) for h in host["tensors"]]
+        mm = (ColumnMatrix.from_device(devs[0], host["d"]) if host["dense"] else
+              ColumnMatrix.from_device_csc(*devs, host["d"]))
+        if host["global_cols"] is not None:
+            mm.mark_shard(host["global_cols"], host["n"])
         ds = LabeledDataset(mm, labels, pb.data.orientation)
         p2 = GlmProblem.build(ds, pb.loss, pb.reg.lam, reg=pb.reg.kind)
         res = run_syscd(p2, cfg)
@@ -447,55 +476,103 @@ def e2e_run(args, wl, world, dist):
     tt = torch.tensor([sorted(times)[len(times) // 2] * len(times)], dtype=torch.float64,
                       device="cuda")
     dist.allreduce_(tt, op="max")
+    h2d = sum(h.numel() * h.element_size() for h in host["tensors"])
+    h2d += labels.size * 8
     return {"value": upd / float(tt), "unit": "updates/s",
-            "h2d_bytes_per_step": int(sum(h.numel() * h.element_size() for h in hosts)
-                                      + labels.size * 8),
-            "d2h_bytes_per_step": int(m.n_cols * 8),
-            "step": f"GlmProblem.build + run_syscd over {cfg.T1} epochs on a host-resident "
-                    "problem (pinned H2D of A and y, column norms, fresh device state, alpha D2H)",
+            "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(pb.n_coordinates * 8),
+            "step": f"GlmProblem.build + run_syscd over {cfg.T1} epochs on host data (pinned H2D "
+                    "of this rank's shard of A and y/labels, column norms, fresh device state, "
+                    "alpha D2H)",
             "seconds_per_step": float(tt) / len(times)}
 
 
-def cpu_baseline(wl, eng, args):
-    from oracle import cpu_baseline as cb
+def oracle_spec(wl, host):
+    """The C++ oracle's view of the same problem (borrowed host arrays)."""
+    from oracle.cpu import CppProblem
+    from paper_1911_07722_b200.objective import KIND_NAMES
     pb = wl.problem
-    kind = ["ridge", "logistic", "lasso", "svm_dual", "logistic_dual"][pb.kind]
-    m = pb.data.matrix
-    sparse = 39 if m.storage_kind == "sparse" else 0
-    r = cb.measure(kind, m.n_rows, pb.reg.lam, eng.a, float(pb.n_coordinates),
-                   budget_s=args.cpu_budget, sparse_nnz=sparse)
-    return {"value": r["updates_per_s"], "unit": "updates/s", "cores": r["cores"],
-            "kind": "port", "sample": r["sample"]}
+    kind = KIND_NAMES[pb.kind]
+    d, n = host["d"], host["n"]
+    dual = pb.is_dual
+    if host["dense"]:
+        return CppProblem(kind, d, n, pb.reg.lam, dense=host["tensors"][0].numpy(),
+                          col_scale=host["labels"] if dual else None,
+                          y=None if dual else host["labels"])
+    cp, ri, va = (t.numpy() for t in host["tensors"])
+    return CppProblem(kind, d, n, pb.reg.lam, csc=(cp, ri, va),
+                      col_scale=host["labels"] if dual else None,
+                      y=None if dual else host["labels"])
+
+
+def oracle_cfg(wl):
+    from oracle.syscd_oracle import OracleConfig
+    c = wl.solver
+    return OracleConfig(K=c.K, P=c.P, bucket_size=c.resolved_bucket_size(), T2=c.T2, T3=c.T3,
+                        T4=c.T4, sampling=c.sampling, repartition=c.repartition, seed=c.seed)
+
+
+def cpu_baseline(wl, host, args, budget_s=20.0):
+    """The C++/OpenMP oracle on the same problem and configuration, on all
+    host cores, for as many whole rounds as fit a ~budget_s sample."""
+    from oracle.cpu import CppOracle
+    o = CppOracle(oracle_spec(wl, host), oracle_cfg(wl))
+    upd, secs, rounds = 0, 0.0, 0
+    while rounds < max(1, args.steps) and (rounds == 0 or secs * (rounds + 1) / rounds < budget_s):
+        u, t = o.round(rounds)
+        upd, secs, rounds = upd + u, secs + t, rounds + 1
+    o.close()
+    return {"value": upd / secs, "unit": "updates/s", "cores": o.threads, "kind": "port",
+            "sample": f"{rounds} round(s) of this workload (same K/P/B/seed/lambda) through the "
+                      "C++/OpenMP fp64 restatement of run_syscd (oracle/syscd_cpu.cpp)",
+            "seconds_per_round": secs / rounds}
 
 
 def run_reference(args):
-    """The reference's CPU path (oracle port) on the host cores, same metric."""
-    import os as _os
-    rank = int(_os.environ.get("RANK", "0"))
-    if rank != 0:
+    """The reference's CPU path on the host cores: the C++/OpenMP fp64
+    restatement of run_syscd (oracle/syscd_cpu.cpp; the reference is pure
+    Python and has no compiled path) on this arm's workload -- same data
+    (the same counter-based generator, run on the GPU before timing), lambda,
+    K, P, B and seed -- one global round per step.  Rank 0 only."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return
-    from oracle import cpu_baseline as cb
-    d, n, kind, lam, P = {0: (20000, 500, "ridge", 1e-3, 4), 1: (28, 2_000_000, "svm_dual", 5e-7, 64),
-                          2: (400_000, 2000, "lasso", 0.08, 148), 3: (1_000_000, 8000, "ridge", 1e-4, 1),
-                          4: (1_000_000, 10_000_000, "logistic_dual", 1e-6, 512)}[args.config]
-    gamma = 1.0 if kind in ("ridge", "lasso") else 1.0 / (lam * n * n)
-    a = gamma * P
-    budget = max(1.0, min(6.0, 120.0 / max(1, args.steps + args.warmup)))
-    vals = []
-    res = None
+    import torch
+    from oracle.cpu import CppOracle
+    from paper_1911_07722_b200.configs import workload
+    torch.cuda.set_device(0)
+    wl = workload(args.config, scale=args.scale, n_gpus=args.gpus)
+    host = host_copy(wl)
+    m = wl.problem.data.matrix
+    m._dev_dense = m._dev_csc = None
+    wl.problem._device = None
+    torch.cuda.empty_cache()
+    o = CppOracle(oracle_spec(wl, host), oracle_cfg(wl))
+    secs, upd = [], 0
     for s in range(args.warmup + args.steps):
-        res = cb.measure(kind, d, lam, a, float(n), budget_s=budget,
-                         sparse_nnz=39 if args.config == 4 else 0, ncols=16)
+        u, t = o.round(s)
         if s >= args.warmup:
-            vals.append(res["updates_per_s"])
-    value = sum(vals) / len(vals)
-    out = {"impl": "reference", "metric": "coord updates/s", "value": value, "unit": "updates/s",
+            secs.append(t)
+            upd += u
+    o.close()
+    value = upd / sum(secs)
+    ms_per_step = 1e3 * sum(secs) / len(secs)
+    c = wl.solver
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "updates/s",
            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": budget * 1e3, "higher_is_better": True, "vs_baseline": None,
-           "dtype": "f64", "data": "synthetic (same distributions)",
-           "config": {"workload": f"config{args.config}", "K": 1, "P": P},
-           "cpu_baseline": {"value": value, "unit": "updates/s", "cores": res["cores"],
-                            "kind": "port", "sample": res["sample"]},
+           "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (the same seeded generator and problem as the ours arm)",
+           "config": {"workload": f"config{args.config}: {wl.name}",
+                      "objective": ["ridge", "logistic", "lasso", "svm_dual",
+                                    "logistic_dual"][wl.problem.kind],
+                      "d": wl.info["d"], "n": wl.info["n"], "lam": wl.info["lam"],
+                      "K": c.K, "P": c.P, "bucket_size": c.resolved_bucket_size(),
+                      "repartition": c.repartition, "seed": c.seed, "epochs_per_step": 1},
+           "a_stream_gbs": wl.a_bytes / (ms_per_step / 1e3) / 1e9,
+           "cpu_baseline": {"value": value, "unit": "updates/s", "cores": o.threads,
+                            "kind": "port",
+                            "sample": f"{args.steps} timed global rounds (after {args.warmup}) of "
+                                      "the workload through oracle/syscd_cpu.cpp, all host cores"},
            "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)

@@ -316,6 +316,27 @@ int syscd_libsvm_fill(const char* buf, int64_t len, int32_t n_threads, double* l
 int syscd_csr_transpose(int64_t n_rows, int64_t n_cols, const int64_t* ptr, const int32_t* idx,
                         const double* vals, int64_t* t_ptr, int32_t* t_idx, double* t_vals);
 
+/* ------------------------------------------------------------------------
+ * Synthetic workload generation (no reference counterpart: the reference
+ * draws its synthetic data with numpy on the host, dataset.py:262-273).
+ * Counter-based (Philox4x32-10): value = f(seed, tag, column id, row), so
+ * every rank generates exactly its own shard's columns in HBM (SURVEY 8(d)
+ * column-block keys) and a sharded job sees the one-GPU matrix.
+ * ------------------------------------------------------------------------ */
+/* out[s*lda + i] = N(0,1) of column cols[s] (cols NULL: s), row i < d; rows
+ * d..lda-1 zero.  lda % 4 == 0. */
+int syscd_gen_normal_cols(uint64_t seed, uint32_t tag, const int64_t* cols, int64_t n_cols,
+                          int64_t d, int64_t lda, float* out, void* stream);
+/* out[t] = N(0,1) (uniform = 0) or U(0,1) (uniform = 1) of id ids[t] (NULL: t) */
+int syscd_gen_ids(uint64_t seed, uint32_t tag, const int64_t* ids, int64_t n, int32_t uniform,
+                  double* out, void* stream);
+/* rows[s*nnz ...] = nnz distinct rows of column cols[s] drawn by inverse CDF
+ * from cdf[0..d) (first nnz distinct draws), sorted ascending; *failed is set
+ * if a column could not collect nnz distinct rows. */
+int syscd_gen_zipf_onehot(uint64_t seed, uint32_t tag, const int64_t* cols, int64_t n_cols,
+                          int64_t d, int32_t nnz, const double* cdf, int32_t* rows,
+                          int32_t* failed, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -114,6 +114,11 @@ SIGNATURES = {
     "syscd_libsvm_scan": (c_i32, [c_vp, c_i64, c_i32, ctypes.POINTER(LibsvmInfo)]),
     "syscd_libsvm_fill": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "syscd_csr_transpose": (c_i32, [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "syscd_gen_normal_cols": (c_i32, [c_u64, ctypes.c_uint32, c_vp, c_i64, c_i64, c_i64, c_vp,
+                                      c_vp]),
+    "syscd_gen_ids": (c_i32, [c_u64, ctypes.c_uint32, c_vp, c_i64, c_i32, c_vp, c_vp]),
+    "syscd_gen_zipf_onehot": (c_i32, [c_u64, ctypes.c_uint32, c_vp, c_i64, c_i64, c_i32, c_vp,
+                                      c_vp, c_vp, c_vp]),
 }
 
 _lib = None

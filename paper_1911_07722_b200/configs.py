@@ -177,135 +177,199 @@ def host_problem(cfg_id, scale=1.0, seed=0):
 
 
 # ---------------------------------------------------------------------------
-# device (torch) generation for full-size runs
+# device generation for full-size runs: counter-based, shard-local
 # ---------------------------------------------------------------------------
-def _device_onehot_rows(n, d, nnz_row, gen, chunk=1 << 20):
-    """n rows of nnz_row distinct features drawn from Zipf(1.1) over d
-    features (inverse-CDF draws, first nnz_row distinct in draw order),
-    returned sorted per row as an (n, nnz_row) int32 CUDA tensor."""
+# Philox stream tags (csrc/datagen.cu): every value is a function of (seed,
+# tag, global column or row id), so rank r generates exactly its store
+# columns and a sharded job holds the one-GPU matrix.
+TAG_A, TAG_W, TAG_WMASK, TAG_NOISE, TAG_FLIP, TAG_ZIPF, TAG_WFEAT, TAG_WFEAT_MASK, TAG_LABEL = \
+    range(1, 10)
+
+
+class _DeviceGen:
+    def __init__(self, cfg_id, seed):
+        self.seed = (1_000_003 * (int(seed) + 1) + 7919 * cfg_id) & ((1 << 64) - 1)
+
+    def _ids(self, ids):
+        import torch
+        if isinstance(ids, int):
+            return None, ids
+        t = torch.as_tensor(ids, dtype=torch.int64).cuda()
+        return t, t.numel()
+
+    def normal_cols(self, cols, d, lda):
+        import torch
+        from .device import _ptr, _stream
+        from ._lib import call
+        t, n = self._ids(cols)
+        out = torch.empty((n, lda), dtype=torch.float32, device="cuda")
+        call("syscd_gen_normal_cols", self.seed, TAG_A, _ptr(t), n, d, lda, _ptr(out), _stream())
+        return out
+
+    def ids(self, ids, tag, uniform=False):
+        import torch
+        from .device import _ptr, _stream
+        from ._lib import call
+        t, n = self._ids(ids)
+        out = torch.empty(n, dtype=torch.float64, device="cuda")
+        call("syscd_gen_ids", self.seed, tag, _ptr(t), n, 1 if uniform else 0, _ptr(out),
+             _stream())
+        return out
+
+    def onehot(self, cols, d, nnz, cdf):
+        import torch
+        from .device import _ptr, _stream
+        from ._lib import call
+        t, n = self._ids(cols)
+        rows = torch.empty((n, nnz), dtype=torch.int32, device="cuda")
+        failed = torch.zeros(1, dtype=torch.int32, device="cuda")
+        call("syscd_gen_zipf_onehot", self.seed, TAG_ZIPF, _ptr(t), n, d, nnz, _ptr(cdf),
+             _ptr(rows), _ptr(failed), _stream())
+        if int(failed.item()):
+            raise RuntimeError("one-hot generation: a column could not draw enough rows")
+        return rows
+
+
+def _chunks(n, ld):
+    step = max(1, (1 << 28) // max(ld, 1))
+    return [(j0, min(n, j0 + step)) for j0 in range(0, n, step)]
+
+
+def shard_arrays(cfg_id, scale=1.0, seed=0, cols=None, dist=None, gen=None, device="cuda"):
+    """The config's data for the global columns `cols` (store order; None =
+    all), generated where it will live.  Quantities that depend on every
+    column (y = A w* + noise, the Lasso lambda, the logistic label threshold)
+    are reduced over `dist`, so every rank ends up with the problem a single
+    GPU builds while holding only its own columns.
+
+    Returns dict(kind, d, n, lam, and either At (n_loc, lda) float32 or csc
+    (col_ptr, row_idx, vals), plus y (length d, primal) or labels (n_loc,
+    dual)).  gen: the column-keyed generator (default: the CUDA kernels)."""
     import torch
-    ranks = torch.arange(1, d + 1, dtype=torch.float64, device="cuda")
-    cdf = torch.cumsum(ranks.pow(-1.1), 0)
-    cdf /= cdf[-1].clone()
-    out = torch.empty((n, nnz_row), dtype=torch.int32, device="cuda")
-    ncand = 4 * nnz_row
-    for r0 in range(0, n, chunk):
-        rows = torch.arange(r0, min(n, r0 + chunk), device="cuda")
-        while rows.numel():
-            R = rows.numel()
-            u = torch.rand((R, ncand), generator=gen, device="cuda", dtype=torch.float64)
-            cand = torch.searchsorted(cdf, u).clamp_(max=d - 1)
-            sv, pos = torch.sort(cand, dim=1, stable=True)
-            first = torch.ones_like(sv, dtype=torch.bool)
-            first[:, 1:] = sv[:, 1:] != sv[:, :-1]
-            keep = torch.zeros_like(first)
-            keep.scatter_(1, pos, first)                 # first occurrence, draw order
-            rank = torch.cumsum(keep.to(torch.int32), 1)
-            ok = rank[:, -1] >= nnz_row
-            sel = keep & (rank <= nnz_row)
-            good = rows[ok]
-            feats = cand[ok][sel[ok]].view(-1, nnz_row)
-            out[good] = torch.sort(feats, dim=1).values.to(torch.int32)
-            rows = rows[~ok]
-    return out
-
-
-def _device_config4(d, n, seed, gen):
-    import torch
-    nnz_row = 39 if d >= 390 else max(1, d // 10)
-    feats = _device_onehot_rows(n, d, nnz_row, gen)
-    w = torch.zeros(d, dtype=torch.float64, device="cuda")
-    k = max(1, d // 100)
-    idx = torch.randperm(d, generator=gen, device="cuda")[:k]
-    w[idx] = 3.0 * torch.randn(k, generator=gen, device="cuda", dtype=torch.float64)
-    score = w[feats.long()].sum(dim=1)
-    lo, hi = float(score.min()) - 20.0, float(score.max()) + 20.0
-    for _ in range(60):  # bias so that the expected positive rate is 25%
-        mid = 0.5 * (lo + hi)
-        if float(torch.sigmoid(score - mid).mean()) > 0.25:
-            lo = mid
-        else:
-            hi = mid
-    prob = torch.sigmoid(score - 0.5 * (lo + hi))
-    y = torch.where(torch.rand(n, generator=gen, device="cuda", dtype=torch.float64) < prob,
-                    1.0, -1.0)
-    col_ptr = torch.arange(0, (n + 1) * nnz_row, nnz_row, dtype=torch.int64, device="cuda")
-    vals = torch.ones(n * nnz_row, dtype=torch.float32, device="cuda")
-    m = ColumnMatrix.from_device_csc(col_ptr, feats.reshape(-1).contiguous(), vals, d)
-    ds = LabeledDataset(m, y.cpu().numpy(), COORDINATES_ARE_EXAMPLES)
-    return GlmProblem.build(ds, SmoothLoss.logistic(), 1e-6)
-
-
-def device_problem(cfg_id, scale=1.0, seed=0):
-    import torch
+    from .device import Dist
+    dist = dist or Dist.single()
     d, n = _dims(cfg_id, scale)
-    gen = torch.Generator(device="cuda")
-    gen.manual_seed(1_000_003 * (seed + 1) + cfg_id)
+    gen = gen or _DeviceGen(cfg_id, seed)
+    sel = None if cols is None else np.asarray(cols, dtype=np.int64)
+    n_loc = n if sel is None else int(sel.size)
+    ids = n if sel is None else sel
+    f64 = dict(dtype=torch.float64, device=device)
     if cfg_id == 4:
-        return _device_config4(d, n, seed, gen)
+        nnz_row = 39 if d >= 390 else max(1, d // 10)
+        ranks = torch.arange(1, d + 1, **f64)
+        cdf = torch.cumsum(ranks.pow(-1.1), 0)
+        cdf /= cdf[-1].clone()
+        rows = gen.onehot(ids, d, nnz_row, cdf)
+        wfeat = 3.0 * gen.ids(d, TAG_WFEAT) * (gen.ids(d, TAG_WFEAT_MASK, uniform=True) < 0.01)
+        score = torch.empty(n_loc, **f64)
+        for j0, j1 in _chunks(n_loc, nnz_row * 64):
+            score[j0:j1] = wfeat[rows[j0:j1].long()].sum(dim=1)
+        ext = torch.tensor([float(score.max()) if n_loc else -1e300,
+                            -float(score.min()) if n_loc else -1e300], **f64)
+        dist.allreduce_(ext, op="max")
+        lo, hi = -float(ext[1]) - 20.0, float(ext[0]) + 20.0
+        for _ in range(60):  # bias so that the expected positive rate is 25%
+            mid = 0.5 * (lo + hi)
+            m = torch.sigmoid(score - mid).sum().reshape(1)
+            if float(dist.allreduce_(m)) / n > 0.25:
+                lo = mid
+            else:
+                hi = mid
+        prob = torch.sigmoid(score - 0.5 * (lo + hi))
+        labels = torch.where(gen.ids(ids, TAG_LABEL, uniform=True) < prob, 1.0, -1.0)
+        col_ptr = torch.arange(0, (n_loc + 1) * nnz_row, nnz_row, dtype=torch.int64,
+                               device=device)
+        vals = torch.ones(n_loc * nnz_row, dtype=torch.float32, device=device)
+        return dict(kind="logistic_dual", d=d, n=n, lam=1e-6,
+                    csc=(col_ptr, rows.reshape(-1), vals), labels=labels)
     ld = padded_ld(d)
-    At = torch.empty((n, ld), dtype=torch.float32, device="cuda")
-    chunk = max(1, (1 << 28) // ld)
-    for j0 in range(0, n, chunk):
-        j1 = min(n, j0 + chunk)
-        At[j0:j1].normal_(generator=gen)
-    if ld > d:
-        At[:, d:] = 0
+    At = gen.normal_cols(ids, d, ld)
     if cfg_id == 1:
-        # columns = samples: normalise each sample (column) to unit norm
+        # columns = samples: each normalised to unit norm; labels from w*
         At[:, :d] /= torch.linalg.norm(At[:, :d], dim=1, keepdim=True)
-        w = torch.randn(d, generator=gen, device="cuda", dtype=torch.float64)
-        y = torch.sign(At[:, :d].double() @ w)
-        y[y == 0] = 1.0
-        flip = torch.rand(n, generator=gen, device="cuda") < 0.1
-        y[flip] = -y[flip]
-        m = ColumnMatrix.from_device(At, d)
-        ds = LabeledDataset(m, y.cpu().numpy(), COORDINATES_ARE_EXAMPLES)
-        return GlmProblem.build(ds, SmoothLoss.hinge(), 1.0 / n)
+        w = gen.ids(d, TAG_W)
+        labels = torch.sign(At[:, :d].double() @ w)
+        labels[labels == 0] = 1.0
+        flip = gen.ids(ids, TAG_FLIP, uniform=True) < 0.1
+        labels[flip] = -labels[flip]
+        return dict(kind="svm_dual", d=d, n=n, lam=1.0 / n, At=At, labels=labels)
     if cfg_id == 2:
-        for j0 in range(0, n, chunk):
-            j1 = min(n, j0 + chunk)
+        for j0, j1 in _chunks(n_loc, ld):
             nrm = torch.linalg.norm(At[j0:j1, :d].double(), dim=1, keepdim=True)
             At[j0:j1, :d] = (At[j0:j1, :d].double() / nrm).float()
-    w = torch.zeros(n, dtype=torch.float64, device="cuda")
-    if cfg_id == 2:
-        k = max(1, int(round(0.05 * n)))
-        idx = torch.randperm(n, generator=gen, device="cuda")[:k]
-        w[idx] = torch.randn(k, generator=gen, device="cuda", dtype=torch.float64)
+        w = gen.ids(ids, TAG_W) * (gen.ids(ids, TAG_WMASK, uniform=True) < 0.05)
         noise = 0.01
     else:
-        w = torch.randn(n, generator=gen, device="cuda", dtype=torch.float64)
+        w = gen.ids(ids, TAG_W)
         noise = 0.1
-    y = torch.zeros(d, dtype=torch.float64, device="cuda")
-    for j0 in range(0, n, chunk):
-        j1 = min(n, j0 + chunk)
+    y = torch.zeros(d, **f64)
+    for j0, j1 in _chunks(n_loc, ld):
         y += At[j0:j1, :d].double().T @ w[j0:j1]
-    y += noise * torch.randn(d, generator=gen, device="cuda", dtype=torch.float64)
-    m = ColumnMatrix.from_device(At, d)
+    dist.allreduce_(y)
+    y += noise * gen.ids(d, TAG_NOISE)
     if cfg_id == 2:
-        aty = torch.empty(n, dtype=torch.float64, device="cuda")
-        for j0 in range(0, n, chunk):
-            j1 = min(n, j0 + chunk)
-            aty[j0:j1] = At[j0:j1, :d].double() @ y
-        lam = LASSO_RATIO * float(aty.abs().max())
-        ds = LabeledDataset(m, y.cpu().numpy(), COORDINATES_ARE_FEATURES)
-        return GlmProblem.build(ds, SmoothLoss.squared_error(), lam, reg="l1")
-    ds = LabeledDataset(m, y.cpu().numpy(), COORDINATES_ARE_FEATURES)
-    return GlmProblem.build(ds, SmoothLoss.squared_error(), 1e-3 if cfg_id == 0 else 1e-4)
+        aty = torch.zeros(1, **f64)
+        for j0, j1 in _chunks(n_loc, ld):
+            aty = torch.maximum(aty, (At[j0:j1, :d].double() @ y).abs().max().reshape(1))
+        lam = LASSO_RATIO * float(dist.allreduce_(aty, op="max"))
+        return dict(kind="lasso", d=d, n=n, lam=lam, At=At, y=y)
+    return dict(kind="ridge", d=d, n=n, lam=1e-3 if cfg_id == 0 else 1e-4, At=At, y=y)
 
 
-def workload(cfg_id, scale=1.0, seed=0, host=None, n_gpus=1, epochs=None):
+def problem_from_arrays(arr, cols=None):
+    """A GlmProblem over device arrays from shard_arrays (or their uploaded
+    copies); cols marks the matrix as this rank's shard."""
+    d, n = arr["d"], arr["n"]
+    if "csc" in arr:
+        m = ColumnMatrix.from_device_csc(*arr["csc"], d)
+    else:
+        m = ColumnMatrix.from_device(arr["At"], d)
+    if cols is not None:
+        m.mark_shard(cols, n)
+    kind = arr["kind"]
+    if kind in ("svm_dual", "logistic_dual"):
+        labels = arr["labels"]
+        labels = labels.cpu().numpy() if hasattr(labels, "cpu") else np.asarray(labels)
+        ds = LabeledDataset(m, labels, COORDINATES_ARE_EXAMPLES)
+        loss = SmoothLoss.hinge() if kind == "svm_dual" else SmoothLoss.logistic()
+        return GlmProblem.build(ds, loss, arr["lam"])
+    y = arr["y"]
+    y = y.cpu().numpy() if hasattr(y, "cpu") else np.asarray(y)
+    ds = LabeledDataset(m, y, COORDINATES_ARE_FEATURES)
+    return GlmProblem.build(ds, SmoothLoss.squared_error(), arr["lam"],
+                            reg="l1" if kind == "lasso" else "l2")
+
+
+def device_problem(cfg_id, scale=1.0, seed=0, cols=None, dist=None):
+    """The config's problem generated in HBM (cols: a rank's shard)."""
+    return problem_from_arrays(shard_arrays(cfg_id, scale, seed, cols, dist), cols)
+
+
+def workload(cfg_id, scale=1.0, seed=0, host=None, n_gpus=1, epochs=None, dist=None):
+    """The config's problem and solver settings.  On a multi-GPU job (dist
+    with world > 1, device generation) each rank generates only its own
+    store columns (the shard of its node groups, sharding.shard_plan)."""
     if host is None:
         host = cfg_id == 0 or (scale < 0.2 and cfg_id != 4) or (cfg_id == 4 and scale < 0.002)
-    pb = host_problem(cfg_id, scale, seed) if host else device_problem(cfg_id, scale, seed)
     solver = default_solver(cfg_id, n_gpus, epochs)
+    d, n = _dims(cfg_id, scale)
+    world = dist.world if dist is not None else 1
+    if host:
+        pb = host_problem(cfg_id, scale, seed)
+    elif world > 1:
+        from .sharding import shard_plan
+        sp = shard_plan(n, solver.resolved_bucket_size(), solver.K, solver.P, solver.seed, world,
+                        dist.rank)
+        pb = device_problem(cfg_id, scale, seed, cols=sp.store_cols, dist=dist)
+    else:
+        pb = device_problem(cfg_id, scale, seed)
     m = pb.data.matrix
     if m.storage_kind == "dense":
-        a_bytes = 4 * m.n_rows * m.n_cols
+        a_bytes = 4 * d * n
     else:
-        nnz = m.nnz()
-        a_bytes = 8 * nnz + 8 * m.n_cols
+        nnz_row = 39 if d >= 390 else max(1, d // 10)
+        a_bytes = (8 * nnz_row + 8) * n if not host else 8 * m.nnz() + 8 * n
     names = {0: "ridge-20000x500", 1: "svm-dual-2Mx28", 2: "lasso-400000x2000",
              3: "ridge-1Mx8000", 4: "logreg-dual-10Mx1M-csc"}
     return Workload(cfg_id, pb, solver, names[cfg_id], a_bytes,
-                    {"d": m.n_rows, "n": m.n_cols, "lam": pb.reg.lam, "scale": scale})
+                    {"d": d, "n": n, "lam": pb.reg.lam, "scale": scale})

@@ -122,6 +122,22 @@ class ColumnMatrix:
         obj._dev_csc = (col_ptr, row_idx, vals)
         return obj
 
+    # -- shards (multi-GPU) ---------------------------------------
+    global_cols = None   # global column id of every held column (None: unsharded)
+    n_cols_global = None
+
+    def mark_shard(self, global_cols, n_cols_global):
+        """Declare that this matrix holds only the columns `global_cols` (in
+        store order) of an n_cols_global-column problem: the rank's shard of
+        the static node partition (partitioning.py:89-96), generated or
+        loaded shard-locally so no rank ever holds the whole matrix."""
+        global_cols = np.asarray(global_cols, dtype=np.int64)
+        if global_cols.shape != (self.n_cols,):
+            raise ValueError("one global column id per held column expected")
+        self.global_cols = global_cols
+        self.n_cols_global = int(n_cols_global)
+        return self
+
     # -- reference accessors (host) ------------------------------------------
     def _host_dense(self):
         if self._dense is None and self._dev_dense is not None:

@@ -144,6 +144,16 @@ class Dist:
         obj.on, obj.rank, obj.world, obj.group = False, 0, 1, None
         return obj
 
+    def allgather(self, t):
+        """[t from rank 0, t from rank 1, ...] (equal shapes)."""
+        if self.world == 1:
+            return [t]
+        import torch
+        import torch.distributed as tdist
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        tdist.all_gather(out, t, group=self.group)
+        return out
+
     def allreduce_(self, t, op="sum"):
         if self.world > 1:
             import torch.distributed as tdist
@@ -162,29 +172,36 @@ class DeviceProblem:
     def __init__(self, problem, store_cols=None, dist=None):
         torch = _torch()
         self.problem = problem
+        m = problem.data.matrix
+        # a shard-local matrix already holds exactly this rank's store columns
+        presharded = m.global_cols is not None
+        if presharded and (store_cols is None or not np.array_equal(store_cols, m.global_cols)):
+            raise ValueError("the problem holds a different shard than this rank's node groups")
         # a full (unsharded) problem has nothing to reduce across ranks
         self.dist = dist if (dist is not None and store_cols is not None) else Dist.single()
-        m = problem.data.matrix
         self.kind = problem.kind
         self.d = m.n_rows
-        self.n_global = m.n_cols
+        self.n_global = problem.n_coordinates
         self.lam = float(problem.reg.lam)
-        self.n_coords = float(m.n_cols)
+        self.n_coords = float(self.n_global)
         self.gamma = float(problem.gamma)
         self.storage = m.storage_kind
         dual = problem.is_dual
         labels = problem.data.labels
-        natural = store_cols is None
-        cols = np.arange(m.n_cols, dtype=np.int64) if natural else np.asarray(store_cols, np.int64)
+        natural = store_cols is None or presharded
+        cols = (np.arange(m.n_cols, dtype=np.int64) if store_cols is None
+                else np.asarray(store_cols, np.int64))
         self.store_cols = cols
         self.n_store = cols.size
+        # rows of the held arrays (labels, norms, device columns) to use
+        local = np.arange(m.n_cols, dtype=np.int64) if natural else cols
         cols_t = None if natural else torch.from_numpy(cols).cuda()
         if self.storage == "dense":
             At = device_dense(m)
             if not natural:
                 At = At.index_select(0, cols_t)
             if dual:
-                yl = torch.from_numpy(labels[cols].astype(np.float32)).cuda()
+                yl = torch.from_numpy(labels[local].astype(np.float32)).cuda()
                 At = At * yl[:, None]
             self.At = At.contiguous()
             self.lda = self.At.shape[1]
@@ -207,14 +224,14 @@ class DeviceProblem:
             if dual:
                 # fold labels into the values: column i becomes y_i x_i
                 cnt = cp[1:] - cp[:-1]
-                ycol = torch.from_numpy(labels[cols].astype(np.float32)).cuda()
+                ycol = torch.from_numpy(labels[local].astype(np.float32)).cuda()
                 va = va * torch.repeat_interleave(ycol, cnt, output_size=int(cp[-1]))
             cp, ri, va = cp.contiguous(), ri.contiguous(), va.contiguous()
             self.csc = (cp, ri, va)
             self.mdev = ("sparse", self.csc)
             self.lda = None
-        sq_full = problem.stats.column_sq_norms
-        self.sq = torch.from_numpy(np.asarray(sq_full, dtype=np.float64)[cols].astype(np.float32)).cuda()
+        sq_held = np.asarray(problem.stats.column_sq_norms, dtype=np.float64)
+        self.sq = torch.from_numpy(sq_held[local].astype(np.float32)).cuda()
         self.y = None if dual else torch.from_numpy(labels.astype(np.float64)).cuda()
         d = self.d
         self.v = torch.zeros(d, dtype=torch.float64, device="cuda")
@@ -306,7 +323,10 @@ class DeviceProblem:
     # -- host-facing helpers (API parity) --------------------------------------
     def upload_alpha(self, alpha_global):
         torch = _torch()
-        a = np.asarray(alpha_global, dtype=np.float64)[self.store_cols].astype(np.float32)
+        a = np.asarray(alpha_global, dtype=np.float64)
+        if a.shape != (self.n_global,):
+            raise ValueError("alpha length does not match coordinate count")
+        a = a[self.store_cols].astype(np.float32)
         return torch.from_numpy(a).cuda()
 
     def objective_host(self, alpha_global):

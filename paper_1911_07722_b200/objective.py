@@ -162,7 +162,8 @@ class GlmProblem:
 
     @property
     def n_coordinates(self):
-        return self.data.matrix.n_cols
+        m = self.data.matrix
+        return m.n_cols_global if m.global_cols is not None else m.n_cols
 
     @property
     def n_shared(self):
@@ -171,8 +172,12 @@ class GlmProblem:
     def device(self):
         """The GPU-resident mirror (created once, cached)."""
         if self._device is None:
-            from .device import DeviceProblem
-            self._device = DeviceProblem(self)
+            from .device import DeviceProblem, Dist
+            m = self.data.matrix
+            if m.global_cols is not None:  # a shard: metrics reduce over the ranks
+                self._device = DeviceProblem(self, store_cols=m.global_cols, dist=Dist())
+            else:
+                self._device = DeviceProblem(self)
         return self._device
 
 

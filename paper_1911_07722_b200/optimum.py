@@ -18,6 +18,7 @@ from .objective import RIDGE
 
 
 def _ridge_cg(problem, rtol=1e-10, max_iter=500):
+    """(x over this rank's store columns, iterations, relative residual)."""
     torch = _torch()
     dp = problem.device()
     d, n = dp.d, dp.n_store
@@ -31,20 +32,24 @@ def _ridge_cg(problem, rtol=1e-10, max_iter=500):
         _rmatvec_raw(md, d, v, out)
         return out + dp.lam * x64
 
+    def dot(a, b):  # over every rank's coordinates (a sharded problem)
+        return float(dp.dist.allreduce_(torch.dot(a, b).reshape(1)))
+
     b = torch.empty(n, dtype=torch.float64, device="cuda")
     _rmatvec_raw(md, d, dp.y, b)
     x = torch.zeros(n, dtype=torch.float64, device="cuda")
     r = b.clone()
     p = r.clone()
-    rs = float(torch.dot(r, r))
-    bnorm = max(float(torch.linalg.norm(b)), 1e-300)
+    rs = dot(r, r)
+    bnorm = max(np.sqrt(dot(b, b)), 1e-300)
+    rs_new = rs
     it = 0
     for it in range(max_iter):
         Ap = normal_op(p)
-        alpha = rs / float(torch.dot(p, Ap))
+        alpha = rs / dot(p, Ap)
         x += alpha * p
         r -= alpha * Ap
-        rs_new = float(torch.dot(r, r))
+        rs_new = dot(r, r)
         if np.sqrt(rs_new) <= rtol * bnorm:
             break
         p = r + (rs_new / rs) * p

@@ -53,10 +53,23 @@ def shard_plan(n, B, K, P, seed, world=1, rank=0):
     np.cumsum([len(nb) for nb in nodes], out=ptr[1:])
     if world == 1:
         return ShardPlan(K, k_local, node0, buckets, ptr, buckets * B, None, n)
+    store_col, store_cols = _bucket_columns(buckets, B, n)
+    return ShardPlan(K, k_local, node0, buckets, ptr, store_col, store_cols, int(store_cols.size))
+
+
+def _bucket_columns(buckets, B, n):
+    """(store column of each bucket's first coordinate, global column of every
+    store column) for buckets laid out back to back in the given order."""
     lo = buckets * B
-    hi = np.minimum(lo + B, n)
-    lens = hi - lo
+    lens = np.minimum(lo + B, n) - lo
     store_col = np.zeros(buckets.size, dtype=np.int64)
     np.cumsum(lens[:-1], out=store_col[1:])
-    store_cols = np.concatenate([np.arange(a, b) for a, b in zip(lo, hi)])
-    return ShardPlan(K, k_local, node0, buckets, ptr, store_col, store_cols, int(lens.sum()))
+    grid = lo[:, None] + np.arange(B, dtype=np.int64)[None, :]
+    store_cols = grid[grid < np.minimum(lo + B, n)[:, None]]
+    return store_col, store_cols
+
+
+def all_store_cols(n, B, K, P, seed, world):
+    """Every rank's store columns (rank order): what an all-gather of the
+    per-rank alpha shards is scattered by."""
+    return [shard_plan(n, B, K, P, seed, world, r).store_cols for r in range(world)]

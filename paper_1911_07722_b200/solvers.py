@@ -151,7 +151,14 @@ class _Engine:
             if problem._device is None:
                 problem._device = DeviceProblem(problem, dist=dist)
             self.dp = problem._device
+        elif problem.data.matrix.global_cols is not None:
+            # shard-local problem: it holds exactly this rank's columns
+            if problem._device is None or not np.array_equal(problem._device.store_cols,
+                                                             sp.store_cols):
+                problem._device = DeviceProblem(problem, store_cols=sp.store_cols, dist=dist)
+            self.dp = problem._device
         else:
+            # full problem on every rank: gather this rank's columns
             self.dp = DeviceProblem(problem, store_cols=sp.store_cols, dist=dist)
         dp = self.dp
         self.single = cfg.K == 1 and cfg.P == 1
@@ -456,15 +463,25 @@ class _Engine:
         return int(torch_unique_count(s)) == tot
 
     def alpha_global(self):
-        """alpha in global coordinate order, fp64 host array."""
+        """alpha in global coordinate order, fp64 host array: an all-gather
+        of the per-rank shards (each rank sends only its n_store values)."""
         dp = self.dp
         if self.dist.world == 1:
             return self.alpha.double().cpu().numpy()
         torch = self.torch
-        full = torch.zeros(dp.n_global, dtype=torch.float64, device="cuda")
-        full[torch.from_numpy(dp.store_cols).cuda()] = self.alpha.double()
-        self.dist.allreduce_(full)
-        return full.cpu().numpy()
+        if getattr(self, "_rank_cols", None) is None:
+            from .sharding import all_store_cols
+            cfg = self.cfg
+            self._rank_cols = all_store_cols(dp.n_global, cfg.resolved_bucket_size(), cfg.K, cfg.P,
+                                             cfg.seed, self.dist.world)
+        m = max(c.size for c in self._rank_cols)
+        buf = torch.zeros(m, dtype=torch.float32, device="cuda")
+        buf[:dp.n_store] = self.alpha
+        parts = self.dist.allgather(buf)
+        full = np.empty(dp.n_global)
+        for cols, part in zip(self._rank_cols, parts):
+            full[cols] = part[:cols.size].double().cpu().numpy()
+        return full
 
 
 class _PlanBuf:

@@ -116,3 +116,64 @@ def test_spec_validation_and_thread_split():
         split_threads("syscd", 6, 4)
     with pytest.raises(ValueError):
         split_threads("sequential", 2, 1)
+
+
+# ---------------------------------------------------------------------------
+# single-coordinate API (host utilities, objective.py:113-232): no device
+# ---------------------------------------------------------------------------
+def _host_pair(kind, d, n, seed):
+    """A tiny problem with host-computed column norms (no GPU) and the same
+    problem for the oracle."""
+    from oracle import syscd_oracle as O
+    from paper_1911_07722_b200 import (COORDINATES_ARE_EXAMPLES, COORDINATES_ARE_FEATURES,
+                                       ColumnMatrix, GlmProblem, LabeledDataset, Regularizer,
+                                       SmoothLoss)
+    from paper_1911_07722_b200.dataset import DatasetStats
+    g = np.random.default_rng(seed)
+    A = g.standard_normal((d, n)).astype(np.float32)
+    sq = (A.astype(np.float64) ** 2).sum(axis=0)
+    stats = DatasetStats(sq, float("nan"), float(sq.max()))
+    if kind in ("ridge", "lasso", "logistic"):
+        y = (g.standard_normal(d) if kind != "logistic"
+             else np.where(g.random(d) < 0.5, -1.0, 1.0))
+        lam = 0.5 if kind != "lasso" else 0.05 * float(np.abs(A.T @ y).max())
+        ds = LabeledDataset(ColumnMatrix(d, n, dense=A), y, COORDINATES_ARE_FEATURES)
+        loss = SmoothLoss.logistic() if kind == "logistic" else SmoothLoss.squared_error()
+        pb = GlmProblem(ds, loss, Regularizer("l1" if kind == "lasso" else "l2", lam), stats)
+        ob = O.OracleProblem(O.OracleMatrix(dense=A.astype(np.float64)), y, kind, lam)
+    else:
+        y = np.where(g.random(n) < 0.5, -1.0, 1.0)
+        lam = 1.0 / n
+        ds = LabeledDataset(ColumnMatrix(d, n, dense=A), y, COORDINATES_ARE_EXAMPLES)
+        loss = SmoothLoss.hinge() if kind == "svm_dual" else SmoothLoss.logistic()
+        pb = GlmProblem(ds, loss, Regularizer("l2", lam), stats)
+        ob = O.OracleProblem(O.OracleMatrix(dense=A.astype(np.float64) * y[None, :]),
+                             np.zeros(d), kind, lam)
+    return pb, ob
+
+
+@pytest.mark.parametrize("kind", ["ridge", "lasso", "svm_dual", "logistic_dual", "logistic"])
+def test_single_coordinate_api_matches_oracle(kind):
+    """exact_coordinate_update / surrogate_coordinate_update against the
+    oracle's per-coordinate steps."""
+    from paper_1911_07722_b200 import (SurrogateContext, exact_coordinate_update,
+                                       surrogate_coordinate_update)
+    pb, ob = _host_pair(kind, 40, 12, seed=21)
+    g = np.random.default_rng(3)
+    alpha = g.uniform(0.05, 0.9, 12) if kind.endswith("dual") else g.standard_normal(12)
+    v = ob.A.matvec(alpha)
+    for j in range(12):
+        got = exact_coordinate_update(pb, j, alpha[j], v)
+        ref = ob.exact_delta(j, alpha[j], v)
+        assert abs(got - ref) <= 1e-5 * max(1.0, abs(ref)), (j, got, ref)
+    if kind == "logistic":
+        return
+    grad = ob.grad(v)
+    a = 4.0 * ob.gamma
+    ctx = SurrogateContext(grad, v, v, a, ob.gamma)
+    v_thread = v + 0.01 * g.standard_normal(v.shape)
+    for j in range(12):
+        got = surrogate_coordinate_update(ctx, pb, j, alpha[j], v_thread)
+        lin = ob.A.col_dot(j, grad) + a * ob.A.col_dot(j, v_thread - v)
+        ref = ob.step(lin, a, j, alpha[j])
+        assert abs(got - ref) <= 1e-5 * max(1.0, abs(ref)), (j, got, ref)

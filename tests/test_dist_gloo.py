@@ -82,3 +82,68 @@ def test_bench_workloads_shard_over_n_gpus(built_lib, n_gpus):
             sp = shard_plan(n, B, cfg.K, cfg.P, cfg.seed, n_gpus, r)
             cols.extend(sp.store_cols.tolist() if sp.store_cols is not None else range(n))
         assert sorted(cols) == list(range(n))
+
+
+SHARD_CASES = [(0, 0.05), (1, 0.0002), (2, 0.01), (3, 0.002), (4, 0.00005)]
+
+
+def _shard_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as tdist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from host_gen import HostGen
+        from paper_1911_07722_b200.configs import _dims, shard_arrays
+        from paper_1911_07722_b200.device import Dist
+        from paper_1911_07722_b200.sharding import shard_plan
+        out = {}
+        for cfg_id, scale in SHARD_CASES:
+            d, n = _dims(cfg_id, scale)
+            sp = shard_plan(n, 4, 2, 1, 0, world, rank)
+            arr = shard_arrays(cfg_id, scale, 0, cols=sp.store_cols, dist=Dist(), gen=HostGen(),
+                               device="cpu")
+            held = arr["csc"][0].numel() - 1 if "csc" in arr else arr["At"].shape[0]
+            mat = (arr["csc"][1].reshape(held, -1) if "csc" in arr else arr["At"]).numpy()
+            out[cfg_id] = dict(cols=sp.store_cols.tolist(), held=int(held), mat=mat.tolist(),
+                               y=arr["y"].tolist() if "y" in arr else None,
+                               labels=arr["labels"].tolist() if "labels" in arr else None,
+                               lam=arr["lam"])
+        q.put((rank, out))
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_two_rank_shard_local_generation(built_lib):
+    """Each rank generates only its own store columns (O(shard) memory: the
+    held matrix has exactly n_store columns); the shards are the columns of
+    the one-process matrix, and y / lambda / labels (reduced over the ranks)
+    equal the one-process values."""
+    from host_gen import HostGen
+    from paper_1911_07722_b200.configs import shard_arrays
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_shard_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for cfg_id, scale in SHARD_CASES:
+        full = shard_arrays(cfg_id, scale, 0, gen=HostGen(), device="cpu")
+        n = full["n"]
+        fm = (full["csc"][1].reshape(n, -1) if "csc" in full else full["At"]).numpy()
+        seen = []
+        for r in range(world):
+            o = out[r][cfg_id]
+            assert o["held"] == len(o["cols"]) < n          # a strict shard
+            np.testing.assert_array_equal(np.array(o["mat"]), fm[o["cols"]])
+            seen += o["cols"]
+            if o["y"] is not None:
+                np.testing.assert_allclose(o["y"], full["y"].numpy(), rtol=1e-12, atol=1e-12)
+            else:
+                np.testing.assert_array_equal(o["labels"], full["labels"].numpy()[o["cols"]])
+            assert abs(o["lam"] - full["lam"]) <= 1e-12 * full["lam"]
+        assert sorted(seen) == list(range(n))

@@ -357,45 +357,3 @@ def test_sparse_exact_logistic_single_worker(cuda):
     res = run_syscd(pb, SolverConfig(seed=2, T1=3, **kw))
     ores = O.run_syscd(ob, O.OracleConfig(seed=2, T1=3, **kw))
     assert_parity(res, ores)
-
-
-@pytest.mark.parametrize("kind", ["ridge", "lasso", "svm_dual", "logistic_dual"])
-def test_single_coordinate_api_matches_oracle(cuda, kind):
-    """exact_coordinate_update / surrogate_coordinate_update (objective.py:
-    113-232) against the oracle's per-coordinate steps."""
-    from paper_1911_07722_b200 import (SurrogateContext, exact_coordinate_update,
-                                       surrogate_coordinate_update)
-    pb, ob = _edge_pair(kind, 40, 12, seed=21)
-    g = np.random.default_rng(3)
-    alpha = g.uniform(0.05, 0.9, 12) if kind.endswith("dual") else g.standard_normal(12)
-    v = ob.A.matvec(alpha)
-    for j in range(12):
-        got = exact_coordinate_update(pb, j, alpha[j], v)
-        ref = ob.exact_delta(j, alpha[j], v)
-        assert abs(got - ref) <= 1e-5 * max(1.0, abs(ref)), (j, got, ref)
-    grad = ob.grad(v)
-    a = 4.0 * ob.gamma
-    ctx = SurrogateContext(grad, v, v, a, ob.gamma)
-    v_thread = v + 0.01 * g.standard_normal(v.shape)
-    for j in range(12):
-        got = surrogate_coordinate_update(ctx, pb, j, alpha[j], v_thread)
-        lin = ob.A.col_dot(j, grad) + a * ob.A.col_dot(j, v_thread - v)
-        ref = ob.step(lin, a, j, alpha[j])  # the oracle step returns delta
-        assert abs(got - ref) <= 1e-5 * max(1.0, abs(ref)), (j, got, ref)
-
-
-def test_single_coordinate_api_logistic(cuda):
-    from paper_1911_07722_b200 import (COORDINATES_ARE_FEATURES, ColumnMatrix, GlmProblem,
-                                       LabeledDataset, SmoothLoss, exact_coordinate_update)
-    g = np.random.default_rng(4)
-    A = g.standard_normal((60, 9)).astype(np.float32)
-    y = np.where(g.random(60) < 0.5, -1.0, 1.0)
-    pb = GlmProblem.build(LabeledDataset(ColumnMatrix(60, 9, dense=A), y,
-                                         COORDINATES_ARE_FEATURES), SmoothLoss.logistic(), 0.3)
-    ob = O.OracleProblem(O.OracleMatrix(dense=A.astype(np.float64)), y, "logistic", 0.3)
-    alpha = g.standard_normal(9)
-    v = ob.A.matvec(alpha)
-    for j in range(9):
-        got = exact_coordinate_update(pb, j, alpha[j], v)
-        ref = ob.exact_delta(j, alpha[j], v)
-        assert abs(got - ref) <= 1e-5 * max(1.0, abs(ref))
