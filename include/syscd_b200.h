@@ -154,8 +154,12 @@ int syscd_dense_epoch(const syscd_dense_epoch_args* e, void* stream);
  * unless its tag is the running partition's, so replicas never need
  * re-zeroing.  Partition p of a call uses tag replica_tag + p: the caller
  * advances replica_tag by n_parts per call (skipping 0; a wrap of the 32-bit
- * tag space needs a re-zero).  delta_v (d) receives the sum of the replicas
- * (zeroed by the call). */
+ * tag space needs a re-zero).  delta_v (d) receives the sum of the replicas.
+ * When n_workers == n_parts (syscd_sparse_epoch_workers returns n_parts
+ * whenever that many workers are resident) worker p runs partition p and the
+ * sum is a fixed ascending-partition reduction of the replica words after
+ * the chains (bitwise reproducible, reduce_replicas solvers.py:112-125);
+ * otherwise it is accumulated with fp32 atomics. */
 typedef struct {
   int32_t kind;
   int64_t d;

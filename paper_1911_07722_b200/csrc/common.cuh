@@ -270,6 +270,16 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef SYSCD_WAIT_HINT
+  // suspend-time hint: the warp sleeps in the barrier instead of re-issuing
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2;\n\t"
+      "@!P bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity), "r"((uint32_t)SYSCD_WAIT_HINT)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred P;\n"
       "WAIT_%=:\n\t"
@@ -277,6 +287,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!P bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
       "r"(parity)
       : "memory");
+#endif
 }
 
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {

@@ -346,7 +346,13 @@ __global__ void __launch_bounds__(Cfg::kThreads, 1) k_dense_epoch(DenseArgs args
         if (lane == 0) mbar_arrive_expect_tx(&xbar[buf], 4u * (uint32_t)C);
       }
       if (dbg && t < 512) args.dbg[t * 6 + 2] = gtimer();
-      mbar_wait(&xbar[buf], (t >> 1) & 1u);
+      // iid: the exchange also hands over rank 0's alpha stores of earlier
+      // steps (a coordinate may be drawn again): the st.async completion is
+      // a cluster-scope release, so wait with cluster-scope acquire
+      if (args.iid)
+        mbar_wait_cluster(&xbar[buf], (t >> 1) & 1u);
+      else
+        mbar_wait(&xbar[buf], (t >> 1) & 1u);
       if (dbg && t < 512) args.dbg[t * 6 + 3] = gtimer();
       float lin;
       {

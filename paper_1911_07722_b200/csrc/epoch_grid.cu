@@ -49,6 +49,9 @@ constexpr int kGRed = 8;      // CTA-reduction slots (events)
 #ifndef SYSCD_GRID_RSLOTS
 #define SYSCD_GRID_RSLOTS 1  // events in flight per reducer warp (2: no gain measured)
 #endif
+#ifndef SYSCD_GRID_CHAINS
+#define SYSCD_GRID_CHAINS 1  // accumulator chains per partial value
+#endif
 #ifndef SYSCD_GRID_SLEEP
 #define SYSCD_GRID_SLEEP 256  // reducer poll back-off (ns)
 #endif
@@ -189,11 +192,11 @@ struct GridLayout {
 // IID: with-replacement sampling (the recently-resolved ring).  Fixing both
 // at compile time takes their branches out of the event loop, whose
 // instruction count bounds this kernel (config 3: 6.51 -> 6.31 ms).
-template <int RR, int BB, int LL, int KIND, bool IID, int NWM>
-__global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
-  // NWM math warps + the producer + NRED reducer warps = 16 warps
+template <int RR, int BB, int LL, int KIND, bool IID, int NWM, int NWT>
+__global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
+  // NWM math warps + the producer + NRED reducer warps = NWT warps
   constexpr int NTC = NWM * 32;
-  constexpr int NRED = 16 - NWM - 1;
+  constexpr int NRED = NWT - NWM - 1;
   constexpr int NRW = NRED;
   static_assert(NRED >= 1, "no reducer warp");
   constexpr int NWC = NTC / 32;
@@ -340,7 +343,9 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
       if ((rel & 31) == 0 && loaded != rel) {
         const int64_t q = s + lane;
         jreg = q < s_end ? A.seq[q] : 0;
-        areg = q < s_end ? A.alpha[jreg] : 0.f;
+        // alpha is written by CTA 0 during the epoch: read it from L2
+        // (ld.cg), never from a possibly stale L1 line (iid redraws)
+        areg = q < s_end ? __ldcg(A.alpha + jreg) : 0.f;
         qreg = q < s_end ? __ldg(A.sq + jreg) : 0.f;
         loaded = rel;
       }
@@ -487,11 +492,21 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
                 }
               }
 #endif
-              float pr[NS];
+              // NCH independent accumulator chains per value (rows r with
+              // r % NCH == h), summed in a fixed order: shorter FMA
+              // dependency chains on the per-event critical path
+              constexpr int NCH = SYSCD_GRID_CHAINS;
+              float prc[NCH][NS];
 #pragma unroll
-              for (int k = 0; k < NS; ++k) pr[k] = 0.f;
+              for (int h = 0; h < NCH; ++h)
+#pragma unroll
+                for (int k = 0; k < NS; ++k) prc[h][k] = 0.f;
+#ifdef SYSCD_GRID_NOMATH  // experiment: data-delivery ceiling (wrong results)
+              prc[0][0] = xr[i][0][0];
+#else
 #pragma unroll
               for (int r = 0; r < RR; ++r) {
+                float* pr = prc[r % NCH];
 #pragma unroll
                 for (int b = 0; b < BB; ++b) {
                   const float xv = xr[i][b][r];
@@ -506,6 +521,14 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
                       pr[Lay::gx(l, b, k)] =
                           fmaf(xv, xr[XS_OLD(l)][k][r], pr[Lay::gx(l, b, k)]);
                 }
+              }
+#endif
+              float pr[NS];
+#pragma unroll
+              for (int k = 0; k < NS; ++k) {
+                pr[k] = prc[0][k];
+#pragma unroll
+                for (int h = 1; h < NCH; ++h) pr[k] += prc[h][k];
               }
               // warp totals (shuffle-transposed: NP-1 + 5-log2(NP) shuffles
               // instead of 5*NS), then warp 0 sums the warps' deposits in
@@ -542,7 +565,9 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
               // ---- resolve block c = e - LL (register slot (i + 1) % NSLOT)
               const int c = e - LL;
               const int64_t cpub = ebase + c;
+#ifndef SYSCD_GRID_NOSYNC  // experiment: no grid dependency (wrong results)
               mbar_wait(&totbar[cpub % kGTot], (uint32_t)((cpub / kGTot) & 1));
+#endif
               GSTAMP(3);
               const float* t = tot + (cpub % kGTot) * kGVal;
               float dcur[BB];
@@ -583,7 +608,7 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
                   }
                   if (isfinite(an)) {
                     dcur[b] = an - aj;
-                    if (cta == 0 && tid == 0) A.alpha[j] = an;
+                    if (cta == 0 && tid == 0) __stcg(A.alpha + j, an);
                   } else if (cta == 0 && tid == 0) {
                     atomicOr(A.status, SYSCD_ENONFINITE);
                   }
@@ -660,23 +685,23 @@ __global__ void __launch_bounds__(512, 1) k_grid_epoch(GridArgs A) {
 // host side
 // ---------------------------------------------------------------------------
 struct GridEntry {
-  int rr, bb, ll, ns, ntc;
+  int rr, bb, ll, ns, ntc, nthreads;
   const void* fn[4][2];  // [ridge / primal logistic, lasso, svm dual, logistic dual][iid]
 };
 
-template <int RR, int BB, int LL, int NWM, int KIND>
+template <int RR, int BB, int LL, int NWM, int NWT, int KIND>
 static void grid_fill(GridEntry& g, int k) {
-  g.fn[k][0] = (const void*)&k_grid_epoch<RR, BB, LL, KIND, false, NWM>;
-  g.fn[k][1] = (const void*)&k_grid_epoch<RR, BB, LL, KIND, true, NWM>;
+  g.fn[k][0] = (const void*)&k_grid_epoch<RR, BB, LL, KIND, false, NWM, NWT>;
+  g.fn[k][1] = (const void*)&k_grid_epoch<RR, BB, LL, KIND, true, NWM, NWT>;
 }
 
-template <int RR, int BB, int LL, int NWM = 13>
+template <int RR, int BB, int LL, int NWM = 13, int NWT = 16>
 static GridEntry make_grid() {
-  GridEntry g{RR, BB, LL, GridLayout<BB, LL>::kNS, NWM * 32, {}};
-  grid_fill<RR, BB, LL, NWM, SYSCD_RIDGE>(g, 0);
-  grid_fill<RR, BB, LL, NWM, SYSCD_LASSO>(g, 1);
-  grid_fill<RR, BB, LL, NWM, SYSCD_SVM_DUAL>(g, 2);
-  grid_fill<RR, BB, LL, NWM, SYSCD_LOGISTIC_DUAL>(g, 3);
+  GridEntry g{RR, BB, LL, GridLayout<BB, LL>::kNS, NWM * 32, NWT * 32, {}};
+  grid_fill<RR, BB, LL, NWM, NWT, SYSCD_RIDGE>(g, 0);
+  grid_fill<RR, BB, LL, NWM, NWT, SYSCD_LASSO>(g, 1);
+  grid_fill<RR, BB, LL, NWM, NWT, SYSCD_SVM_DUAL>(g, 2);
+  grid_fill<RR, BB, LL, NWM, NWT, SYSCD_LOGISTIC_DUAL>(g, 3);
   return g;
 }
 
@@ -692,6 +717,12 @@ static GridEntry g_grid_table[] = {
     make_grid<8, 2, 2>(),
     make_grid<12, 2, 1>(),
     make_grid<16, 1, 3, 14>(),
+    // fewer, wider math warps: the per-warp event overhead (waits, warp
+    // reductions, the redundant step) is paid by 8 warps instead of 14
+    make_grid<36, 1, 3, 6, 8>(),
+    make_grid<24, 1, 3, 9, 12>(),
+    make_grid<22, 1, 3, 10, 12>(),
+    make_grid<27, 1, 2, 8, 12>(),
 };
 constexpr int kGridTable = sizeof(g_grid_table) / sizeof(g_grid_table[0]);
 
@@ -703,24 +734,31 @@ int grid_choose(int64_t d, int* idx, int* G, int* stages, size_t* smem_out) {
   SYSCD_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   SYSCD_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const char* force = getenv("SYSCD_GRID_CFG");
+  // the entry with the most CTAs (row slices) that still fits one wave wins;
+  // ties go to the earlier entry (SYSCD_GRID_CFG=<index> overrides)
+  constexpr int kNQ = 5;  // reducer lanes gather kNQ CTAs each (k_grid_epoch NQ)
+  int best = -1, best_g = 0, best_s = 0;
   for (int i = 0; i < kGridTable; ++i) {
     if (force && atoi(force) != i) continue;
-    if (!force) {  // first entry for each RR only
-      bool first = true;
-      for (int k = 0; k < i; ++k) first &= g_grid_table[k].rr != g_grid_table[i].rr;
-      if (!first) continue;
-    }
     const int rows = g_grid_table[i].ntc * g_grid_table[i].rr;
     const int64_t g = (d + rows - 1) / rows;
-    if (g > sms) continue;
+    if (g > sms || g > 32 * kNQ) continue;
     const size_t fixed = grid_smem(0, rows, g_grid_table[i].ns).total + 1024;
     int s = (int)(((size_t)optin - 1024 - fixed) / ((size_t)rows * 4));
     s = std::min(s, 8);
     if (s < g_grid_table[i].bb + 2) continue;
-    *idx = i;
-    *G = (int)g;
-    *stages = s;
-    *smem_out = grid_smem(s, rows, g_grid_table[i].ns).total;
+    if (g > best_g) {
+      best = i;
+      best_g = (int)g;
+      best_s = s;
+    }
+  }
+  if (best >= 0) {
+    const int rows = g_grid_table[best].ntc * g_grid_table[best].rr;
+    *idx = best;
+    *G = best_g;
+    *stages = best_s;
+    *smem_out = grid_smem(best_s, rows, g_grid_table[best].ns).total;
     return SYSCD_OK;
   }
   set_error("no grid configuration covers d=%lld", (long long)d);
@@ -773,7 +811,7 @@ int grid_launch(const syscd_dense_epoch_args* e, void* workspace, int64_t ws_byt
   SYSCD_CUDA_TRY(cudaMemsetAsync(A.recs, 0, grid_workspace_bytes(G), stream));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(G, 1, 1);
-  cfg.blockDim = dim3(512, 1, 1);
+  cfg.blockDim = dim3(ge.nthreads, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];

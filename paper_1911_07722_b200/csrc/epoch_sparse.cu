@@ -29,8 +29,14 @@
 // same hash, so most probes hit the first slot).  A column longer than the
 // chunk capacity is streamed by the consumer on its own.
 //
-// The node sum uses fp32 atomics across workers, so this kernel is
-// deterministic only up to that summation order (documented in DESIGN.md).
+// Node sum.  When every partition has its own worker (n_parts <= resident
+// workers, e.g. config 4: 512 partitions), worker g runs exactly partition g
+// and its tagged replica words ARE that partition's dv at the end of the
+// round; k_sparse_node_sum then adds them in ascending partition order
+// (fixed order, bitwise reproducible; the reference's reduce_replicas,
+// solvers.py:112-125,393).  With more partitions than workers a worker's
+// replica region is reused, so the node sum falls back to fp32 atomics
+// (deterministic only up to their order).
 #include <algorithm>
 
 #include "common.cuh"
@@ -56,6 +62,7 @@ struct SparseArgs {
   float* delta_v;
   int32_t* status;
   uint32_t tag0;
+  int32_t one_part;  // worker g runs partition g; node sum reduced after the kernel
   unsigned long long* prof;  // debug: per-worker phase cycles (nullptr = off)
 };
 
@@ -336,7 +343,12 @@ __global__ void __launch_bounds__(64) k_sparse_epoch(SparseArgs A, int W) {
   }
   __syncthreads();
   int64_t p_lo, p_hi;
-  worker_parts(A.wp, A.n_parts, W, g, &p_lo, &p_hi);
+  if (A.one_part) {
+    p_lo = g;
+    p_hi = g + 1;
+  } else {
+    worker_parts(A.wp, A.n_parts, W, g, &p_lo, &p_hi);
+  }
   unsigned long long* dv = A.dv_work + (int64_t)g * A.d;
   const float a = A.a;
   unsigned long long ph[4] = {0, 0, 0, 0};
@@ -362,7 +374,7 @@ __global__ void __launch_bounds__(64) k_sparse_epoch(SparseArgs A, int W) {
           const float cv = B.acc[h];
           if (cv != 0.f) {
             rep_store(dv, r, tag, B.dvold[h] + cv);
-            red_add_f32(A.delta_v + r, cv);
+            if (!A.one_part) red_add_f32(A.delta_v + r, cv);
           }
           B.key[h] = kEmpty;
         }
@@ -443,7 +455,7 @@ __global__ void __launch_bounds__(64) k_sparse_epoch(SparseArgs A, int W) {
             const float c = delta * A.vals[e];
             const float nv = rep_load_cg(dv, i, tag) + c;
             rep_store(dv, i, tag, nv);
-            red_add_f32(A.delta_v + i, c);
+            if (!A.one_part) red_add_f32(A.delta_v + i, c);
             if (patch) pc_patch(N, i, nv, a);
           }
         }
@@ -531,6 +543,21 @@ __global__ void __launch_bounds__(64) k_sparse_epoch(SparseArgs A, int W) {
     for (int i = 0; i < 4; ++i) A.prof[(int64_t)g * 8 + warp * 4 + i] = ph[i];
 }
 
+// delta_v[r] = sum over partitions p (ascending) of replica word (p, r) when
+// it carries partition p's tag (else that partition left row r untouched)
+__global__ void k_sparse_node_sum(const unsigned long long* __restrict__ dv_work, int32_t n_parts,
+                                  int64_t d, uint32_t tag0, float* __restrict__ delta_v) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < d;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int p = 0; p < n_parts; ++p) {
+      const unsigned long long x = __ldcs(dv_work + (int64_t)p * d + r);
+      if ((uint32_t)(x >> 32) == tag0 + (uint32_t)p) s += (double)__uint_as_float((uint32_t)x);
+    }
+    delta_v[r] = (float)s;
+  }
+}
+
 static unsigned long long* g_sparse_prof = nullptr;
 
 // one resident wave of workers (a worker owns whole partitions; more
@@ -602,8 +629,9 @@ extern "C" int syscd_sparse_epoch(const syscd_sparse_epoch_args* e, void* stream
   A.delta_v = e->delta_v;
   A.status = e->status;
   A.prof = g_sparse_prof;
+  A.one_part = W == e->n_parts ? 1 : 0;
   cudaStream_t s = (cudaStream_t)stream;
-  SYSCD_CUDA_TRY(cudaMemsetAsync(e->delta_v, 0, e->d * sizeof(float), s));
+  if (!A.one_part) SYSCD_CUDA_TRY(cudaMemsetAsync(e->delta_v, 0, e->d * sizeof(float), s));
   const size_t smem = sizeof(PcSmem);
   void (*fn)(SparseArgs, int) = e->kind == SYSCD_LASSO          ? k_sparse_epoch<SYSCD_LASSO>
                                 : e->kind == SYSCD_SVM_DUAL        ? k_sparse_epoch<SYSCD_SVM_DUAL>
@@ -613,5 +641,14 @@ extern "C" int syscd_sparse_epoch(const syscd_sparse_epoch_args* e, void* stream
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   fn<<<W, 64, smem, s>>>(A, W);
   SYSCD_CUDA_TRY(cudaGetLastError());
+  if (A.one_part) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t blocks = std::min<int64_t>((e->d + 255) / 256, (int64_t)sms * 8);
+    k_sparse_node_sum<<<(int)blocks, 256, 0, s>>>(A.dv_work, e->n_parts, e->d, A.tag0,
+                                                  e->delta_v);
+    SYSCD_CUDA_TRY(cudaGetLastError());
+  }
   return SYSCD_OK;
 }

@@ -101,6 +101,10 @@ def test_config4_logistic_dual_full_size_parity(cuda):
     _gap_parity(res, ores)
     assert np.all((res.alpha >= 0) & (res.alpha <= 1))  # fp32 alpha may round onto 0 or 1
     assert all(m.updates == 10_000_000 for m in res.metrics[1:])
+    # one worker per partition: the node sum is a fixed-order reduction of
+    # the replicas (no atomics), so the run is bitwise reproducible
+    res2 = _run(wl, 2)
+    assert np.array_equal(res.alpha, res2.alpha)
 
 
 def test_config0_full_size_verify(cuda):
