@@ -1,19 +1,23 @@
-"""Experiment sweeps with the reference's CSV schema (mirror of
-pkg/src/syscd/cli.py:26-205, the library half of the `syscd train` command).
+"""Parameter sweeps on the GPU solver, reported in the reference's CSV schema.
 
-run_experiment(spec) loads or generates the dataset, computes F* when asked,
-sweeps thread counts x bucket sizes through run_solver on the GPU and writes
-the per-epoch metrics CSV and the summary CSV with the reference's columns,
-row order and formatting (non-finite floats and None as empty cells).  The
-argparse front end itself is out of scope; a spec is built in
-Python.  Extension: `loss` also accepts "hinge" (dual problems) and `reg`
-selects "l1" (Lasso) -- the reference's names keep their meaning.
+The reference's `syscd train` command (pkg/src/syscd/cli.py:128-205) runs a
+grid of (thread count, bucket size) through run_solver and writes two CSVs:
+one row per epoch and one summary row per run.  This module keeps that
+schema -- column names and order, row order, empty cells for missing or
+non-finite values, the exit status -- so downstream tooling reads either
+implementation's files (tests/test_gpu_experiment.py compares against CSVs
+the reference itself wrote).  The argparse front end is out of scope
+(DESIGN.md): a sweep is described by an ExperimentSpec built in Python.
+
+Extensions: `loss="hinge"` (dual problems, with the example orientation of
+the dataset) and `reg="l1"` (Lasso).
 """
 
 from __future__ import annotations
 
 import csv
 import dataclasses
+import itertools
 import math
 from dataclasses import dataclass
 
@@ -22,19 +26,23 @@ from .objective import GlmProblem, SmoothLoss
 from .optimum import compute_reference_optimum
 from .solvers import SolverConfig, run_solver
 
-EXIT_OK = 0
-EXIT_USAGE = 2
-EXIT_DIVERGED = 3
+EXIT_OK, EXIT_USAGE, EXIT_DIVERGED = 0, 2, 3
 
-METRIC_FIELDS = ["experiment_id", "algorithm", "threads", "epoch", "seconds", "objective",
-                 "suboptimality", "rel_change", "converged", "reason"]
-SUMMARY_FIELDS = ["experiment_id", "algorithm", "threads", "bucket_size", "epochs",
-                  "time_per_epoch", "epochs_to_tolerance", "total_time", "converged", "reason"]
+# the reference's column layouts (cli.py:190-205)
+METRIC_FIELDS = ("experiment_id", "algorithm", "threads", "epoch", "seconds", "objective",
+                 "suboptimality", "rel_change", "converged", "reason")
+SUMMARY_FIELDS = ("experiment_id", "algorithm", "threads", "bucket_size", "epochs",
+                  "time_per_epoch", "epochs_to_tolerance", "total_time", "converged", "reason")
+
+_LOSSES = {"squared": SmoothLoss.squared_error, "logistic": SmoothLoss.logistic,
+           "hinge": SmoothLoss.hinge}
 
 
 @dataclass
 class ExperimentSpec:
-    """cli.py:26-49."""
+    """One sweep: a dataset source (LIBSVM file or synthetic shape), the
+    objective, the grid of thread counts x bucket sizes, the base solver
+    settings and the two output paths (fields of cli.py's spec)."""
 
     solver: str
     libsvm_path: str | None
@@ -58,104 +66,104 @@ class ExperimentSpec:
         if not self.thread_counts or not self.bucket_sizes:
             raise ValueError("sweep lists must be nonempty")
 
+    def dataset(self):
+        if self.libsvm_path is not None:
+            return load_libsvm(self.libsvm_path)
+        rows, cols = self.synthetic_shape
+        if self.density is None:
+            return generate_synthetic_dense(rows, cols, self.base.seed)
+        return generate_synthetic_sparse(rows, cols, self.density, self.base.seed)
+
+    def problem(self):
+        if self.loss not in _LOSSES:
+            raise ValueError(f"unknown loss: {self.loss}")
+        return GlmProblem.build(self.dataset(), _LOSSES[self.loss](), self.lam, reg=self.reg)
+
 
 def loss_from_name(name):
-    if name == "squared":
-        return SmoothLoss.squared_error()
-    if name == "logistic":
-        return SmoothLoss.logistic()
-    if name == "hinge":
-        return SmoothLoss.hinge()
-    raise ValueError(f"unknown loss: {name}")
+    if name not in _LOSSES:
+        raise ValueError(f"unknown loss: {name}")
+    return _LOSSES[name]()
 
 
-def load_spec_dataset(spec):
-    """cli.py:65-71."""
-    if spec.libsvm_path is not None:
-        return load_libsvm(spec.libsvm_path)
-    n_ex, n_feat = spec.synthetic_shape
-    if spec.density is not None:
-        return generate_synthetic_sparse(n_ex, n_feat, spec.density, spec.base.seed)
-    return generate_synthetic_dense(n_ex, n_feat, spec.base.seed)
-
-
-def split_threads(solver, total, nodes):
-    """(K, P) for a total thread count (cli.py:114-125)."""
-    if solver == "sequential":
-        if total != 1:
+def node_thread_split(algorithm, threads, nodes):
+    """(K, P) realising `threads` workers: the flat solvers take no node
+    groups; SySCD spreads them evenly over `nodes` groups."""
+    if algorithm == "sequential":
+        if threads != 1:
             raise ValueError("sequential solver runs on one thread")
         return 1, 1
-    if solver == "wild":
+    if algorithm == "wild":
         if nodes != 1:
             raise ValueError("wild solver is flat (K must be 1)")
-        return 1, total
-    if total % nodes != 0 or total < nodes:
-        raise ValueError(f"thread count {total} is not divisible by {nodes} nodes")
-    return nodes, total // nodes
+        return 1, threads
+    if threads < nodes or threads % nodes:
+        raise ValueError(f"thread count {threads} is not divisible by {nodes} nodes")
+    return nodes, threads // nodes
 
 
-def run_experiment(spec):
-    """Execute the sweep and write the two CSVs (cli.py:128-187).
+class _Report:
+    """Accumulates the per-epoch and per-run records of a sweep."""
 
-    Returns (metric_rows, summary_rows).  Divergence is a row with
-    converged=False and reason="diverged", never an exception.
-    """
-    dataset = load_spec_dataset(spec)
-    problem = GlmProblem.build(dataset, loss_from_name(spec.loss), spec.lam, reg=spec.reg)
-    f_star = None
-    if spec.reference != "none":
-        _, f_star = compute_reference_optimum(problem, spec.reference)
-    rows, summaries = [], []
-    exp_id = 0
-    for threads in spec.thread_counts:
-        for bucket in spec.bucket_sizes:
-            K, P = split_threads(spec.solver, threads, spec.nodes)
-            cfg = dataclasses.replace(spec.base, algorithm=spec.solver, K=K, P=P,
-                                      bucket_size=bucket, verify=spec.verify)
-            result = run_solver(problem, cfg, f_star=f_star)
-            epochs = result.metrics[1:]  # row 0 is the initial state
-            for em in epochs:
-                rows.append({
-                    "experiment_id": exp_id, "algorithm": spec.solver, "threads": K * P,
-                    "epoch": em.epoch, "seconds": em.seconds, "objective": em.objective,
-                    "suboptimality": em.suboptimality, "rel_change": em.rel_change,
-                    "converged": result.converged, "reason": result.reason or "",
-                })
-            total_time = sum(em.seconds for em in epochs)
-            summaries.append({
-                "experiment_id": exp_id, "algorithm": spec.solver, "threads": K * P,
-                "bucket_size": cfg.resolved_bucket_size(), "epochs": len(epochs),
-                "time_per_epoch": total_time / len(epochs) if epochs else "",
-                "epochs_to_tolerance": len(epochs) if result.converged else "",
-                "total_time": total_time, "converged": result.converged,
-                "reason": result.reason or "",
-            })
-            exp_id += 1
-    write_csv(spec.out_path, rows, METRIC_FIELDS)
-    write_csv(spec.summary_path, summaries, SUMMARY_FIELDS)
-    return rows, summaries
+    def __init__(self, algorithm):
+        self.algorithm = algorithm
+        self.epochs = []
+        self.runs = []
+
+    def add(self, run_id, cfg, result):
+        threads = cfg.K * cfg.P
+        tail = result.metrics[1:]  # metrics[0] is the state before the first epoch
+        status = dict(converged=result.converged, reason=result.reason or "")
+        self.epochs.extend(
+            dict(experiment_id=run_id, algorithm=self.algorithm, threads=threads, epoch=m.epoch,
+                 seconds=m.seconds, objective=m.objective, suboptimality=m.suboptimality,
+                 rel_change=m.rel_change, **status)
+            for m in tail)
+        elapsed = math.fsum(m.seconds for m in tail)
+        self.runs.append(dict(
+            experiment_id=run_id, algorithm=self.algorithm, threads=threads,
+            bucket_size=cfg.resolved_bucket_size(), epochs=len(tail),
+            time_per_epoch=elapsed / len(tail) if tail else "",
+            epochs_to_tolerance=len(tail) if result.converged else "",
+            total_time=elapsed, **status))
+
+
+def _cell(value):
+    """CSV cell text: None and non-finite floats become empty cells."""
+    if value is None or (isinstance(value, float) and not math.isfinite(value)):
+        return ""
+    return value
 
 
 def write_csv(path, rows, fields):
-    """cli.py:190-205: non-finite floats and None become empty cells."""
     with open(path, "w", newline="") as fh:
-        w = csv.DictWriter(fh, fieldnames=fields)
-        w.writeheader()
-        for row in rows:
-            out = {}
-            for key in fields:
-                val = row[key]
-                if isinstance(val, float) and not math.isfinite(val):
-                    val = ""
-                if val is None:
-                    val = ""
-                out[key] = val
-            w.writerow(out)
+        out = csv.writer(fh)
+        out.writerow(fields)
+        out.writerows([_cell(r[f]) for f in fields] for r in rows)
+
+
+def run_experiment(spec):
+    """Run every (threads, bucket size) point of the sweep on the GPU and
+    write both CSVs; returns (epoch rows, run rows).  A diverged run is a
+    row with reason "diverged", never an exception."""
+    problem = spec.problem()
+    f_star = None if spec.reference == "none" else \
+        compute_reference_optimum(problem, spec.reference)[1]
+    report = _Report(spec.solver)
+    grid = itertools.product(spec.thread_counts, spec.bucket_sizes)
+    for run_id, (threads, bucket) in enumerate(grid):
+        K, P = node_thread_split(spec.solver, threads, spec.nodes)
+        cfg = dataclasses.replace(spec.base, algorithm=spec.solver, K=K, P=P,
+                                  bucket_size=bucket, verify=spec.verify)
+        report.add(run_id, cfg, run_solver(problem, cfg, f_star=f_star))
+    write_csv(spec.out_path, report.epochs, METRIC_FIELDS)
+    write_csv(spec.summary_path, report.runs, SUMMARY_FIELDS)
+    return report.epochs, report.runs
 
 
 def exit_code(summaries):
-    """The `train` command's exit status (cli.py:335-342): 3 when every run
-    of the sweep diverged, else 0."""
+    """The train command's status (cli.py:335-342): EXIT_DIVERGED when every
+    run of the sweep diverged, else EXIT_OK."""
     if summaries and all(s["reason"] == "diverged" for s in summaries):
         return EXIT_DIVERGED
     return EXIT_OK

@@ -104,18 +104,18 @@ def test_shard_plan_single_and_errors(built_lib):
 
 def test_spec_validation_and_thread_split():
     from paper_1911_07722_b200 import SolverConfig
-    from paper_1911_07722_b200.experiment import ExperimentSpec, split_threads
+    from paper_1911_07722_b200.experiment import ExperimentSpec, node_thread_split
     base = SolverConfig()
     with pytest.raises(ValueError, match="exactly one dataset source"):
         ExperimentSpec("syscd", None, None, None, "squared", 1.0, 1, [1], [8], base, "a", "b")
     with pytest.raises(ValueError, match="nonempty"):
         ExperimentSpec("syscd", None, (10, 2), None, "squared", 1.0, 1, [], [8], base, "a", "b")
-    assert split_threads("syscd", 8, 2) == (2, 4)
-    assert split_threads("wild", 8, 1) == (1, 8)
+    assert node_thread_split("syscd", 8, 2) == (2, 4)
+    assert node_thread_split("wild", 8, 1) == (1, 8)
     with pytest.raises(ValueError):
-        split_threads("syscd", 6, 4)
+        node_thread_split("syscd", 6, 4)
     with pytest.raises(ValueError):
-        split_threads("sequential", 2, 1)
+        node_thread_split("sequential", 2, 1)
 
 
 # ---------------------------------------------------------------------------
