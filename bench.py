@@ -372,7 +372,9 @@ def time_to_target(wl, args, dist=None, target=1e-4, max_epochs=2000):
     pb = wl.problem
     dual = pb.is_dual
     if dual:
-        cap = {1: 300, 4: 60}.get(wl.cfg_id, 200)
+        # config 1 reaches the 1e-4 certificate in ~1700 epochs (~3 s); config
+        # 4 converges ~1/t (scripts/ttt_scan.py): report the best after 300
+        cap = {1: 2500, 4: 300}.get(wl.cfg_id, 200)
         cfg = dataclasses.replace(wl.solver, T1=cap, metrics_every=max(1, cap // 30),
                                   compute_gap=True)
         res = run_syscd(pb, cfg, dist=dist)

@@ -718,11 +718,11 @@ static GridEntry g_grid_table[] = {
     make_grid<12, 2, 1>(),
     make_grid<16, 1, 3, 14>(),
     // fewer, wider math warps: the per-warp event overhead (waits, warp
-    // reductions, the redundant step) is paid by 8 warps instead of 14
+    // reductions, the redundant step) is paid by 6 warps instead of 14
+    // (config 3: 6.34 -> 5.80 ms).  Measured and not kept:
+    // <24,1,3,9 of 12 warps> 5.89, <22,1,3,10/12> 7.46, <27,1,2,8/12> 10.8,
+    // <36,1,4,6/8> 7.44 ms (255 registers).
     make_grid<36, 1, 3, 6, 8>(),
-    make_grid<24, 1, 3, 9, 12>(),
-    make_grid<22, 1, 3, 10, 12>(),
-    make_grid<27, 1, 2, 8, 12>(),
 };
 constexpr int kGridTable = sizeof(g_grid_table) / sizeof(g_grid_table[0]);
 
