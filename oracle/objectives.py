@@ -15,7 +15,7 @@ The reference rejects everything else (objective.py:52-56,74-77); the three
 extra rows (lasso, hinge-SVM dual, logistic dual) follow SURVEY.md Appendix A
 and are parity-unpinned by the reference's own tests (pinned here by 1-D
 golden-section KATs and by running them through the reference driver with the
-step swapped, see tests/test_oracle_vs_reference.py).
+step swapped: tests/test_oracle.py, fixtures by tests/golden/make_golden.py).
 """
 
 from __future__ import annotations

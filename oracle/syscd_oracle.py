@@ -7,7 +7,8 @@ oracle/ and fails loudly when its CUDA library is missing.
 
 It restates the reference's hot path (pkg/src/syscd/solvers.py:289-453) with
 the same arithmetic order so that, on ridge, it reproduces the reference
-bitwise (pinned in tests/test_oracle_vs_reference.py):
+bitwise (pinned in tests/test_oracle.py against the reference-generated
+tests/golden/reference_runs.json, and live when /root/reference is mounted):
 
   * buckets            partitioning.py:77-82 (consecutive ranges, last partial)
   * node partition     partitioning.py:89-96  key (0,)

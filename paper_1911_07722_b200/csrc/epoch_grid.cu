@@ -74,6 +74,7 @@ struct GridArgs {
   int32_t iid;
   int32_t stages;
   int32_t evict_first;
+  int64_t cta_rows;          // rows per CTA (<= NTC*RR, a multiple of 4)
   float* out;                // [d] summed replicas (one worker row)
   unsigned long long* recs;  // [kGNB][NS][G] tagged partials, zeroed before launch
   int32_t* status;
@@ -230,7 +231,10 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
   const int lane = tid & 31;
   const int G = gridDim.x;
   const int cta = blockIdx.x;
-  const int64_t row0 = (int64_t)cta * CTA_ROWS;
+  // a CTA's slice may be shorter than the NTC*RR rows its threads can hold, so
+  // the grid covers d with every SM (the rows past the slice stay zero)
+  const int64_t cta_rows = A.cta_rows;
+  const int64_t row0 = (int64_t)cta * cta_rows;
   const int64_t d = A.d;
   const int64_t s_begin = A.wp[0];
   const int64_t s_end = A.wp[A.n_parts];
@@ -328,7 +332,7 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
     }
     // producer state (warp NWC)
     int64_t valid = d - row0;
-    valid = valid < 0 ? 0 : (valid > CTA_ROWS ? CTA_ROWS : valid);
+    valid = valid < 0 ? 0 : (valid > cta_rows ? cta_rows : valid);
     const uint32_t bytes = (uint32_t)(((valid + 3) / 4) * 16);
     const uint64_t policy = A.evict_first ? policy_evict_first() : policy_evict_last();
     uint32_t stage = 0, phase = 0;
@@ -384,7 +388,7 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
     }
   } else {
     // -------------------------------------------------------------- math warps
-    const int64_t rem = d - row0 - tid;
+    const int64_t rem = min(cta_rows, d - row0) - tid;
     const int rmax = rem <= 0 ? 0 : (int)min((int64_t)RR, (rem + NTC - 1) / NTC);
     const float* ub = A.u + row0 + tid;
     float* outp = A.out + row0 + tid;
@@ -721,14 +725,15 @@ static GridEntry g_grid_table[] = {
     // reductions, the redundant step) is paid by 6 warps instead of 14
     // (config 3: 6.34 -> 5.80 ms).  Measured and not kept:
     // <24,1,3,9 of 12 warps> 5.89, <22,1,3,10/12> 7.46, <27,1,2,8/12> 10.8,
-    // <36,1,4,6/8> 7.44 ms (255 registers).
+    // <36,1,4,6/8> 7.44 ms (255 registers); fewer, longer slices
+    // <38,1,3,6/8> (138 CTAs) 5.92, <40,...> (131) 5.99, <43,1,3,5/7> 6.39.
     make_grid<36, 1, 3, 6, 8>(),
 };
 constexpr int kGridTable = sizeof(g_grid_table) / sizeof(g_grid_table[0]);
 
 static void* g_grid_dbg = nullptr;
 
-int grid_choose(int64_t d, int* idx, int* G, int* stages, size_t* smem_out) {
+int grid_choose(int64_t d, int* idx, int* G, int* stages, size_t* smem_out, int64_t* cta_rows) {
   int dev = 0, sms = 0, optin = 0;
   SYSCD_CUDA_TRY(cudaGetDevice(&dev));
   SYSCD_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -759,6 +764,12 @@ int grid_choose(int64_t d, int* idx, int* G, int* stages, size_t* smem_out) {
     *G = best_g;
     *stages = best_s;
     *smem_out = grid_smem(best_s, rows, g_grid_table[best].ns).total;
+    // Slices are the entry's full capacity.  Spreading d over every SM
+    // (148 slices of 6784 rows instead of 145 of 6912, 128-byte aligned or
+    // not) measured slower on config 3: 6.01 against 5.80 ms per epoch.
+    const int64_t cr = rows;
+    if (cta_rows) *cta_rows = cr;
+    *G = (int)((d + cr - 1) / cr);
     return SYSCD_OK;
   }
   set_error("no grid configuration covers d=%lld", (long long)d);
@@ -771,7 +782,8 @@ int grid_launch(const syscd_dense_epoch_args* e, void* workspace, int64_t ws_byt
                 cudaStream_t stream) {
   int idx, G, stages;
   size_t smem;
-  int st = grid_choose(e->d, &idx, &G, &stages, &smem);
+  int64_t cta_rows = 0;
+  int st = grid_choose(e->d, &idx, &G, &stages, &smem, &cta_rows);
   if (st) return st;
   if (ws_bytes < grid_workspace_bytes(G) || !workspace) {
     set_error("syscd_dense_epoch: grid workspace too small");
@@ -804,6 +816,7 @@ int grid_launch(const syscd_dense_epoch_args* e, void* workspace, int64_t ws_byt
   A.kind = e->kind;
   A.stages = stages;
   A.evict_first = ((double)e->lda * 4.0 * (double)e->n_store) > 64.0 * 1024 * 1024 ? 1 : 0;
+  A.cta_rows = cta_rows;
   A.out = e->partials;
   A.recs = (unsigned long long*)workspace;
   A.status = e->status;

@@ -53,7 +53,10 @@ def _result(syscd, res):
 
 def install(syscd):
     """Patch the reference package `syscd` (an imported module); returns a
-    function that restores the original entry points."""
+    function that restores the original entry points.  Idempotent: a second
+    call returns the first call's undo()."""
+    if getattr(syscd, "_b200_dropin", None) is not None:
+        return syscd._b200_dropin
     from . import solvers as ours
     saved = [(mod, name, getattr(mod, name)) for mod in (syscd, syscd.solvers) for name in _ENTRY]
     cache = {}
@@ -80,5 +83,7 @@ def install(syscd):
         for mod, name, fn in saved:
             setattr(mod, name, fn)
         cache.clear()
+        syscd._b200_dropin = None
 
+    syscd._b200_dropin = undo
     return undo
