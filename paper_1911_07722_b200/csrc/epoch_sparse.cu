@@ -37,6 +37,8 @@
 // solvers.py:112-125,393).  With more partitions than workers a worker's
 // replica region is reused, so the node sum falls back to fp32 atomics
 // (deterministic only up to their order).
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "common.cuh"
@@ -63,6 +65,7 @@ struct SparseArgs {
   int32_t* status;
   uint32_t tag0;
   int32_t one_part;  // worker g runs partition g; node sum reduced after the kernel
+  int32_t hot;       // rows [0, hot) of the replica stay in shared memory (0: none)
   unsigned long long* prof;  // debug: per-worker phase cycles (nullptr = off)
 };
 
@@ -141,9 +144,12 @@ __device__ __forceinline__ int pc_find(const PcBuf& T, int r) {
 }
 
 // Stage the chunk starting at c0 of the partition into B.
+// Slots: a nonzero's slot is its row r when r < H (the worker's resident
+// hot rows, shared by both buffers) and H + h for hash slot h otherwise.
 __device__ __forceinline__ void pc_produce(const SparseArgs& A, PcBuf& B, int lane, int64_t c0,
                                            int64_t s1, uint32_t tag,
                                            const unsigned long long* dv, int* m_out) {
+  const int H = A.hot;
   const float a = A.a;
   const int64_t sl = c0 + lane;
   int j = 0, nnz = 0;
@@ -239,6 +245,10 @@ __device__ __forceinline__ void pc_produce(const SparseArgs& A, PcBuf& B, int la
     for (int q = 0; q < 8; ++q) {
       const int e = lane + 32 * (k0 + q);
       rq[q] = e < nz ? B.row[e] : kEmpty;
+      if (rq[q] != kEmpty && rq[q] < H) {  // resident hot row: no table entry
+        B.slot[e] = (short)rq[q];
+        rq[q] = kEmpty;
+      }
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -260,7 +270,7 @@ __device__ __forceinline__ void pc_produce(const SparseArgs& A, PcBuf& B, int la
         const unsigned fh = pc_fhash(rq[q]);
         atomicOr(&B.filt[fh >> 5], 1u << (fh & 31));
       }
-      B.slot[e] = (short)h;
+      B.slot[e] = (short)(H + (int)h);
     }
   }
   // distinct-slot list (warp prefix over the owners' counts)
@@ -286,7 +296,7 @@ __device__ __forceinline__ void pc_produce(const SparseArgs& A, PcBuf& B, int la
       if ((own >> k) & 1u) {
         const int e = lane + 32 * k;
         const int r = B.row[e];
-        hh[q] = B.slot[e];
+        hh[q] = B.slot[e] - H;
         uu[q] = __ldg(A.u + r);
         dw[q] = __ldcg(dv + r);
       }
@@ -416,6 +426,25 @@ __global__ void __launch_bounds__(64) k_sparse_epoch(SparseArgs A, int W) {
     }
   } else {
     // ---------------- consumer ----------------
+    // Hot rows [0, H): the running partition's b = u + a dv and its dv stay
+    // resident in shared memory for the whole partition (no gather, patch or
+    // writeback per chunk); at a partition change they are written back as
+    // replica words (and to the node sum in the atomic mode).  With rows in
+    // descending frequency order (config 4's Zipf features are) this keeps
+    // most of a chunk's distinct rows off HBM.
+    const int H = A.hot;
+    float* hot_b = reinterpret_cast<float*>(smem_raw + sizeof(PcSmem));
+    float* hot_acc = hot_b + H;
+    uint32_t hot_tag = 0;  // partition whose hot rows are resident (0: none)
+    auto hot_flush = [&]() {
+      for (int r = lane; r < H; r += 32) {
+        const float cv = hot_acc[r];
+        if (cv != 0.f) {
+          rep_store(dv, r, hot_tag, cv);
+          if (!A.one_part) red_add_f32(A.delta_v + r, cv);
+        }
+      }
+    };
     for (int k = 0;; ++k) {
       const int bi = k & 1;
       mbar_wait(&S.full[bi], (k >> 1) & 1);
@@ -425,6 +454,15 @@ __global__ void __launch_bounds__(64) k_sparse_epoch(SparseArgs A, int W) {
       const uint32_t tag = C.tag;
       const int nb = (k + 1) & 1;
       PcBuf& N = S.buf[nb];
+      if (H > 0 && tag != hot_tag) {  // a new partition: swap the hot rows
+        if (hot_tag != 0) hot_flush();
+        for (int r = lane; r < H; r += 32) {
+          hot_b[r] = __ldg(A.u + r);
+          hot_acc[r] = 0.f;
+        }
+        hot_tag = tag;
+        __syncwarp();
+      }
       PC_PHASE(0);
       if (m == 0) {
         // a single long column, streamed with the replica read and written in
@@ -437,7 +475,8 @@ __global__ void __launch_bounds__(64) k_sparse_epoch(SparseArgs A, int W) {
         float part = 0.f;
         for (int64_t e = a0 + lane; e < a1; e += 32) {
           const int i = A.ri[e];
-          part = fmaf(A.vals[e], fmaf(a, rep_load_cg(dv, i, tag), A.u[i]), part);
+          const float bv = i < H ? hot_b[i] : fmaf(a, rep_load_cg(dv, i, tag), A.u[i]);
+          part = fmaf(A.vals[e], bv, part);
         }
         part = warp_sum(part);
         const float aj = *(volatile float*)(A.alpha + jj);
@@ -453,6 +492,11 @@ __global__ void __launch_bounds__(64) k_sparse_epoch(SparseArgs A, int W) {
           for (int64_t e = a0 + lane; e < a1; e += 32) {
             const int i = A.ri[e];
             const float c = delta * A.vals[e];
+            if (i < H) {
+              hot_b[i] = fmaf(a, c, hot_b[i]);
+              hot_acc[i] += c;
+              continue;
+            }
             const float nv = rep_load_cg(dv, i, tag) + c;
             rep_store(dv, i, tag, nv);
             if (!A.one_part) red_add_f32(A.delta_v + i, c);
@@ -467,7 +511,10 @@ __global__ void __launch_bounds__(64) k_sparse_epoch(SparseArgs A, int W) {
         for (int t = 0; t < m; ++t) {
           const int b0 = C.col_pre[t], b1 = C.col_pre[t + 1];
           float part = 0.f;
-          for (int e = b0 + lane; e < b1; e += 32) part = fmaf(C.val[e], C.b[C.slot[e]], part);
+          for (int e = b0 + lane; e < b1; e += 32) {
+            const int sl = C.slot[e];
+            part = fmaf(C.val[e], sl < H ? hot_b[sl] : C.b[sl - H], part);
+          }
           const float lin = warp_sum(part);
           const int jt = C.col_j[t];
           const float aj = C.alpha_c[t];
@@ -480,10 +527,12 @@ __global__ void __launch_bounds__(64) k_sparse_epoch(SparseArgs A, int W) {
           }
           if (delta != 0.f) {
             for (int e = b0 + lane; e < b1; e += 32) {
-              const int h = C.slot[e];
+              const int sl = C.slot[e];
               const float c = delta * C.val[e];
-              C.b[h] = fmaf(a, c, C.b[h]);
-              C.acc[h] += c;
+              float* bp = sl < H ? hot_b + sl : C.b + (sl - H);
+              float* ap = sl < H ? hot_acc + sl : C.acc + (sl - H);
+              *bp = fmaf(a, c, *bp);
+              *ap += c;
             }
           }
           if (lane < m && lane > t && C.col_j[lane] == jt) C.alpha_c[lane] = aj + delta;
@@ -537,6 +586,7 @@ __global__ void __launch_bounds__(64) k_sparse_epoch(SparseArgs A, int W) {
       if (lane == 0) mbar_arrive(&S.empty[bi]);
       PC_PHASE(3);
     }
+    if (hot_tag != 0) hot_flush();
   }
 #undef PC_PHASE
   if (A.prof && lane == 0)
@@ -560,20 +610,41 @@ __global__ void k_sparse_node_sum(const unsigned long long* __restrict__ dv_work
 
 static unsigned long long* g_sparse_prof = nullptr;
 
-// one resident wave of workers (a worker owns whole partitions; more
-// workers than fit would only queue)
-static int sparse_workers(int32_t n_parts) {
-  int dev = 0, sms = 148, per_sm = 4;
-  if (cudaGetDevice(&dev) == cudaSuccess) {
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    // every instance has the same shape: the logistic-dual one (most registers) decides
-    if (cudaFuncSetAttribute(k_sparse_epoch<SYSCD_LOGISTIC_DUAL>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(PcSmem)) == cudaSuccess)
+// One resident wave of workers (a worker owns whole partitions; more workers
+// than fit would only queue) and the hot-row count: the largest H whose
+// shared memory (8 H bytes per worker) still lets every partition have its
+// own worker -- the deterministic one-partition-per-worker mode -- else none.
+struct SparsePlan {
+  int workers;
+  int hot;
+};
+
+static int sparse_per_sm(size_t smem) {
+  int per_sm = 0;
+  const void* fn = (const void*)k_sparse_epoch<SYSCD_LOGISTIC_DUAL>;  // most registers
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess ||
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sparse_epoch<SYSCD_LOGISTIC_DUAL>,
-                                                    64, sizeof(PcSmem));
+                                                    64, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
   }
-  return std::max(1, std::min((int)n_parts, sms * std::max(per_sm, 1)));
+  return per_sm;
+}
+
+static SparsePlan sparse_plan(int64_t d, int32_t n_parts) {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const char* force = getenv("SYSCD_SPARSE_HOT");  // experiments: fixed H
+  for (int H = 16384; H >= 32; H /= 2) {  // (H <= d/4: some rows stay hashed)
+    if (force && atoi(force) != H) continue;
+    if (4 * (int64_t)H > d) continue;
+    const int per_sm = sparse_per_sm(sizeof(PcSmem) + 8 * (size_t)H);
+    if (per_sm > 0 && (int64_t)sms * per_sm >= n_parts) return {n_parts, H};
+  }
+  const int per_sm = std::max(1, sparse_per_sm(sizeof(PcSmem)));
+  return {std::max(1, std::min((int)n_parts, sms * per_sm)), 0};
 }
 
 }  // namespace syscd
@@ -593,7 +664,7 @@ extern "C" int syscd_sparse_epoch_workers(int64_t d, int32_t n_parts, int32_t* n
     set_error("syscd_sparse_epoch_workers: invalid arguments");
     return SYSCD_EINVAL;
   }
-  *n_workers = sparse_workers(n_parts);
+  *n_workers = sparse_plan(d, n_parts).workers;
   return SYSCD_OK;
 }
 
@@ -630,9 +701,11 @@ extern "C" int syscd_sparse_epoch(const syscd_sparse_epoch_args* e, void* stream
   A.status = e->status;
   A.prof = g_sparse_prof;
   A.one_part = W == e->n_parts ? 1 : 0;
+  const SparsePlan plan = sparse_plan(e->d, e->n_parts);
+  A.hot = plan.workers == W ? plan.hot : 0;
   cudaStream_t s = (cudaStream_t)stream;
   if (!A.one_part) SYSCD_CUDA_TRY(cudaMemsetAsync(e->delta_v, 0, e->d * sizeof(float), s));
-  const size_t smem = sizeof(PcSmem);
+  const size_t smem = sizeof(PcSmem) + 8 * (size_t)A.hot;
   void (*fn)(SparseArgs, int) = e->kind == SYSCD_LASSO          ? k_sparse_epoch<SYSCD_LASSO>
                                 : e->kind == SYSCD_SVM_DUAL        ? k_sparse_epoch<SYSCD_SVM_DUAL>
                                 : e->kind == SYSCD_LOGISTIC_DUAL   ? k_sparse_epoch<SYSCD_LOGISTIC_DUAL>
