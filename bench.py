@@ -518,7 +518,7 @@ def cpu_baseline(wl, host, args, budget_s=20.0):
     """The C++/OpenMP oracle on the same problem and configuration, on all
     host cores, for as many whole rounds as fit a ~budget_s sample."""
     from oracle.cpu import CppOracle
-    o = CppOracle(oracle_spec(wl, host), oracle_cfg(wl))
+    o = CppOracle(oracle_spec(wl, host), oracle_cfg(wl), threads=len(os.sched_getaffinity(0)))
     upd, secs, rounds = 0, 0.0, 0
     while rounds < max(1, args.steps) and (rounds == 0 or secs * (rounds + 1) / rounds < budget_s):
         u, t = o.round(rounds)
@@ -548,7 +548,8 @@ def run_reference(args):
     m._dev_dense = m._dev_csc = None
     wl.problem._device = None
     torch.cuda.empty_cache()
-    o = CppOracle(oracle_spec(wl, host), oracle_cfg(wl))
+    # all host cores (torchrun exports OMP_NUM_THREADS=1 to every rank)
+    o = CppOracle(oracle_spec(wl, host), oracle_cfg(wl), threads=len(os.sched_getaffinity(0)))
     secs, upd = [], 0
     for s in range(args.warmup + args.steps):
         u, t = o.round(s)

@@ -28,6 +28,7 @@ def _ridge_cg(problem, rtol=1e-10, max_iter=500):
 
     def normal_op(x64):
         _matvec_raw(md, d, x64.float(), v, work)
+        dp.dist.allreduce_(v)  # a sharded problem: A x sums every rank's columns
         out = torch.empty(n, dtype=torch.float64, device="cuda")
         _rmatvec_raw(md, d, v, out)
         return out + dp.lam * x64

@@ -68,3 +68,59 @@ def test_two_rank_parity(cuda, cfg_id, scale, kw):
     assert u0 == [r.updates for r in ores.rows]
     na = np.linalg.norm(ores.alpha)
     assert np.linalg.norm(np.array(a0) - ores.alpha) / na < 1e-3
+
+
+def _shard_rank(rank, world, port, q):
+    import torch
+    import torch.distributed as tdist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1911_07722_b200 import SolverConfig, run_syscd
+        from paper_1911_07722_b200.configs import workload
+        from paper_1911_07722_b200.device import Dist
+        from paper_1911_07722_b200.optimum import _ridge_cg
+        dist = Dist()
+        wl = workload(3, scale=0.02, host=False, n_gpus=world, dist=dist)
+        m = wl.problem.data.matrix
+        x, _, res = _ridge_cg(wl.problem)
+        f_star = wl.problem.device().objective(x.float())
+        r = run_syscd(wl.problem, SolverConfig(K=world, P=1, bucket_size=8, T1=3, seed=0),
+                      dist=dist)
+        q.put((rank, m.n_cols, int(m.global_cols.size), f_star, res, r.alpha.tolist(),
+               [mm.objective for mm in r.metrics]))
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_two_rank_shard_local_problem(cuda):
+    """Shard-local generation on the GPU (each rank holds only its columns),
+    the distributed CG optimum and a K=2 solve agree with one process
+    holding the whole problem."""
+    from paper_1911_07722_b200 import SolverConfig, run_syscd
+    from paper_1911_07722_b200.configs import workload
+    from paper_1911_07722_b200.optimum import _ridge_cg
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_shard_rank, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    full = workload(3, scale=0.02, host=False)
+    n = full.problem.n_coordinates
+    assert sum(o[1] for o in out) == n and all(o[1] < n for o in out)
+    x, _, _ = _ridge_cg(full.problem)
+    f_star = full.problem.device().objective(x.float())
+    for o in out:
+        assert abs(o[3] - f_star) <= 1e-9 * abs(f_star), (o[3], f_star)
+    ref = run_syscd(full.problem, SolverConfig(K=2, P=1, bucket_size=8, T1=3, seed=0))
+    (_, _, _, _, _, a0, o0), (_, _, _, _, _, a1, o1) = out
+    assert a0 == a1 and o0 == o1
+    r = np.array([m.objective for m in ref.metrics])
+    assert np.max(np.abs(np.array(o0) - r) / np.abs(r)) < 1e-6
+    assert np.linalg.norm(np.array(a0) - ref.alpha) <= 1e-5 * np.linalg.norm(ref.alpha)
