@@ -55,8 +55,11 @@ CASES = [
     (2, 0.25, dict(K=1, P=16, bucket_size=3, T1=2)),
     (2, 0.1, dict(K=1, P=6, bucket_size=5, sampling="iid", T3=4, T4=6, T1=2)),
     (3, 0.05, dict(K=2, P=4, bucket_size=8, T1=2)),
-    # iid on the grid-wide kernel: repeats inside the prefetch window
+    # iid on the grid-wide kernel: repeats inside the prefetch window, and
+    # (T3=60 buckets drawn from 150) coordinates redrawn far more than the 64
+    # columns the recently-resolved ring covers (alpha then comes from L2)
     (3, 0.15, dict(K=1, P=1, bucket_size=8, sampling="iid", T3=12, T4=8, T1=3)),
+    (3, 0.15, dict(K=1, P=1, bucket_size=8, sampling="iid", T3=60, T4=8, T1=2)),
     (2, 0.5, dict(K=1, P=2, bucket_size=4, sampling="iid", T3=20, T4=6, T1=2)),
 ]
 
