@@ -304,7 +304,9 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
       }
       if (lane == 0) {
 #ifdef SYSCD_TRACE
+#ifndef SYSCD_TRACE_LIGHT
         if (A.dbg && cta == 0 && r < 1024) A.dbg[r * 8 + 5] = gtimer_g();
+#endif
         if (A.dbg && r < 1024) A.dbg[8192 + 1024 * 160 + r * 160 + cta] = gtimer_g();
 #endif
         mbar_arrive(&totbar[r % kGTot]);
@@ -429,7 +431,7 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
         for (int i = 0; i < NSLOT; ++i) {
           const int e = e0 + i;  // e % NSLOT == i: register slot of block e
           if (e < nb + LL) {
-#ifdef SYSCD_TRACE
+#if defined(SYSCD_TRACE) && !defined(SYSCD_TRACE_LIGHT)
             const bool dbg = A.dbg && cta == 0 && tid == 0 && p == 0 && e < 1024;
             // all-CTA stamps (thread 0 of each CTA): [e][cta][k]
             unsigned long long* da = (A.dbg && tid == 0 && p == 0 && e < 1024)
@@ -641,7 +643,7 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
               }
             }
             GSTAMP(4);
-#if defined(SYSCD_TRACE) || defined(SYSCD_GRID_DCHK)
+#if (defined(SYSCD_TRACE) && !defined(SYSCD_TRACE_LIGHT)) || defined(SYSCD_GRID_DCHK)
             if (A.dbg && tid == 0 && e >= LL && ebase + e - LL < 8192) {
               // every event's first delta per CTA (divergence check)
               A.dbg[8192 + 2 * 1024 * 160 + 1024 * 160 * 8 + (ebase + e - LL) * 160 + cta] =
@@ -649,7 +651,7 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
                   __float_as_uint(tot[((ebase + e - LL) % kGTot) * kGVal]);
             }
 #endif
-#ifdef SYSCD_TRACE
+#if defined(SYSCD_TRACE) && !defined(SYSCD_TRACE_LIGHT)
             if (da && e >= LL) {
               const float* tt = tot + ((ebase + e - LL) % kGTot) * kGVal;
               da[5] = ((unsigned long long)__float_as_uint(dh[0][0]) << 32) | __float_as_uint(tt[0]);
