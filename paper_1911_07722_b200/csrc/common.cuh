@@ -80,7 +80,17 @@ __device__ __forceinline__ bool logistic_dual_fast(double lin, double aq, double
     const float w = rcp_approx(1.f + e);
     float ns;
     if (tail) {
+#ifndef SYSCD_TAIL_CONTRACTION
+      // Newton on F(s) = s - n (Cl - aq sigma(s)): F' = 1 + n aq sigma (1 -
+      // sigma) >= 1 and F is convex in the tail, so from s0 = n Cl (F > 0)
+      // the iterates decrease monotonically onto the root, quadratically
+      const float sig = sp >= 0.f ? w : e * w;
+      const float F = sp - nf * (Clf - aqf * sig);
+      const float dF = fmaf(nf * aqf * sig, 1.f - sig, 1.f);
+      ns = sp - F * rcp_approx(dF);
+#else
       ns = nf * (Clf - aqf * (sp >= 0.f ? w : e * w));
+#endif
     } else {
       const float R = Clf - sp * inv_nf;
       if (R > 0.f) {
@@ -98,7 +108,11 @@ __device__ __forceinline__ bool logistic_dual_fast(double lin, double aq, double
     // (and the fp64 polish squares it again; its residual check guards the
     // rest): exit one iteration earlier than waiting for a 1e-5 step.  The
     // tail contraction converges linearly and keeps the 1e-5 test.
+#ifndef SYSCD_TAIL_CONTRACTION
+    if (fabsf(step) <= 4e-3f * fmaxf(1.f, fabsf(sp))) {
+#else
     if (fabsf(step) <= (tail ? 1e-5f : 4e-3f) * fmaxf(1.f, fabsf(sp))) {
+#endif
       conv = true;
       break;
     }

@@ -508,35 +508,85 @@ __global__ void __launch_bounds__(64) k_sparse_epoch(SparseArgs A, int W) {
       } else {
         if (A.iid && lane < m) C.alpha_c[lane] = *(volatile float*)(A.alpha + C.col_j[lane]);
         __syncwarp();
+        // Columns of up to 64 nonzeros (two per lane) take a register path:
+        // the next column's slots and values are loaded while this column's
+        // dot reduces, b and acc are read once and written back from
+        // registers (a column's rows are distinct, so no lane races another).
+        int ps0 = 0, ps1 = 0, pb0 = C.col_pre[0], pb1 = C.col_pre[1];
+        float pv0 = 0.f, pv1 = 0.f;
+        if (pb0 + lane < pb1) { ps0 = C.slot[pb0 + lane]; pv0 = C.val[pb0 + lane]; }
+        if (pb0 + 32 + lane < pb1) { ps1 = C.slot[pb0 + 32 + lane]; pv1 = C.val[pb0 + 32 + lane]; }
         for (int t = 0; t < m; ++t) {
-          const int b0 = C.col_pre[t], b1 = C.col_pre[t + 1];
-          float part = 0.f;
-          for (int e = b0 + lane; e < b1; e += 32) {
-            const int sl = C.slot[e];
-            part = fmaf(C.val[e], sl < H ? hot_b[sl] : C.b[sl - H], part);
-          }
-          const float lin = warp_sum(part);
+          const int b0 = pb0, b1 = pb1;
           const int jt = C.col_j[t];
           const float aj = C.alpha_c[t];
-          const float an = sparse_step<KIND>(A, lin, aj, C.q_c[t]);
+          const float qt = C.q_c[t];
           float delta = 0.f;
-          if (isfinite(an)) {
-            delta = an - aj;
-          } else if (lane == 0) {
-            atomicOr(A.status, SYSCD_ENONFINITE);
-          }
-          if (delta != 0.f) {
+          bool ok;
+          if (b1 - b0 <= 64) {
+            const bool in0 = b0 + lane < b1, in1 = b0 + 32 + lane < b1;
+            const int s0 = ps0, s1 = ps1;
+            const float v0 = pv0, v1 = pv1;
+            float* bp0 = s0 < H ? hot_b + s0 : C.b + (s0 - H);
+            float* ap0 = s0 < H ? hot_acc + s0 : C.acc + (s0 - H);
+            float* bp1 = s1 < H ? hot_b + s1 : C.b + (s1 - H);
+            float* ap1 = s1 < H ? hot_acc + s1 : C.acc + (s1 - H);
+            const float bv0 = in0 ? *bp0 : 0.f, bv1 = in1 ? *bp1 : 0.f;
+            const float av0 = in0 ? *ap0 : 0.f, av1 = in1 ? *ap1 : 0.f;
+            // the next column's layout (static) under the reduction's latency
+            if (t + 1 < m) {
+              pb0 = b1;
+              pb1 = C.col_pre[t + 2];
+              ps0 = ps1 = 0;
+              if (pb0 + lane < pb1) { ps0 = C.slot[pb0 + lane]; pv0 = C.val[pb0 + lane]; }
+              if (pb0 + 32 + lane < pb1) { ps1 = C.slot[pb0 + 32 + lane]; pv1 = C.val[pb0 + 32 + lane]; }
+            }
+            const float lin = warp_sum(fmaf(v1, bv1, v0 * bv0));
+            const float an = sparse_step<KIND>(A, lin, aj, qt);
+            ok = isfinite(an);
+            if (ok) delta = an - aj;
+            if (delta != 0.f) {
+              const float c0 = delta * v0, c1 = delta * v1;
+              if (in0) {
+                *bp0 = fmaf(a, c0, bv0);
+                *ap0 = av0 + c0;
+              }
+              if (in1) {
+                *bp1 = fmaf(a, c1, bv1);
+                *ap1 = av1 + c1;
+              }
+            }
+          } else {
+            float part = 0.f;
             for (int e = b0 + lane; e < b1; e += 32) {
               const int sl = C.slot[e];
-              const float c = delta * C.val[e];
-              float* bp = sl < H ? hot_b + sl : C.b + (sl - H);
-              float* ap = sl < H ? hot_acc + sl : C.acc + (sl - H);
-              *bp = fmaf(a, c, *bp);
-              *ap += c;
+              part = fmaf(C.val[e], sl < H ? hot_b[sl] : C.b[sl - H], part);
+            }
+            const float lin = warp_sum(part);
+            const float an = sparse_step<KIND>(A, lin, aj, qt);
+            ok = isfinite(an);
+            if (ok) delta = an - aj;
+            if (delta != 0.f) {
+              for (int e = b0 + lane; e < b1; e += 32) {
+                const int sl = C.slot[e];
+                const float c = delta * C.val[e];
+                float* bp = sl < H ? hot_b + sl : C.b + (sl - H);
+                float* ap = sl < H ? hot_acc + sl : C.acc + (sl - H);
+                *bp = fmaf(a, c, *bp);
+                *ap += c;
+              }
+            }
+            if (t + 1 < m) {
+              pb0 = b1;
+              pb1 = C.col_pre[t + 2];
+              ps0 = ps1 = 0;
+              if (pb0 + lane < pb1) { ps0 = C.slot[pb0 + lane]; pv0 = C.val[pb0 + lane]; }
+              if (pb0 + 32 + lane < pb1) { ps1 = C.slot[pb0 + 32 + lane]; pv1 = C.val[pb0 + 32 + lane]; }
             }
           }
+          if (!ok && lane == 0) atomicOr(A.status, SYSCD_ENONFINITE);
           if (lane < m && lane > t && C.col_j[lane] == jt) C.alpha_c[lane] = aj + delta;
-          if (lane == 0 && isfinite(an)) A.alpha[jt] = aj + delta;
+          if (lane == 0 && ok) A.alpha[jt] = aj + delta;
           __syncwarp();
         }
         PC_PHASE(1);
