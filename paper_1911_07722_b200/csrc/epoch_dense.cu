@@ -504,6 +504,10 @@ static KernelEntry g_table[] = {
     make_entry<32, 1, 1>(),  make_entry<96, 1, 1>(),  make_entry<224, 2, 1>(),
     make_entry<224, 4, 1>(), make_entry<480, 4, 1>(), make_entry<480, 4, 2>(),
     make_entry<480, 4, 4>(), make_entry<480, 8, 4>(), make_entry<480, 9, 6>(),
+    // (the grid kernel's fewer-wider-warps trick does not carry over: 7
+    // consumer warps x 117 rows, 233 registers, ran config 2 at 1.00 ms
+    // against 0.61 -- both passes read the staged slice from shared memory,
+    // and 7 warps cannot keep enough loads in flight)
 };
 static std::mutex g_table_mu;
 constexpr int kTableSize = sizeof(g_table) / sizeof(g_table[0]);
@@ -579,7 +583,9 @@ static int choose(int64_t d, int32_t n_parts, Choice* out) {
   const size_t budget = (size_t)smem_optin - 1024;
   double best = 1e300;
   Choice bc = {-1, 0, 0, 0, 0, 0};
+  const char* force = getenv("SYSCD_DENSE_CFG");  // experiments: one table entry
   for (int i = 0; i < kTableSize; ++i) {
+    if (force && atoi(force) != i) continue;
     KernelEntry& e = g_table[i];
     const int rows = entry_rows(e);
     const int C = (int)((d + rows - 1) / rows);
