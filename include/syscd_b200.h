@@ -255,6 +255,11 @@ int syscd_apply_dv(int32_t kind, int64_t d, const float* dv, double* v, const do
 /* u = grad f(v) + drift * (v_node - v)   (solvers.py:379-382 for T2 > 1) */
 int syscd_grad(int32_t kind, int64_t d, const double* v, const double* y, double lam,
                double n_coords, const double* v_node, double drift, float* u, void* stream);
+/* T2 > 1 node rounds (solvers.py:384-393,423): acc = (first ? 0 : acc) +
+ * (v_node - v) over the local nodes in ascending order, then v += acc. */
+int syscd_node_delta(int64_t d, const double* v_node, const double* v, double* acc,
+                     int32_t first, void* stream);
+int syscd_vec_add(int64_t d, double* v, const double* acc, void* stream);
 /* fp64 certificate point for the duality gap: primal kinds w = grad f(v),
  * dual kinds w = v / (lam n). */
 int syscd_dual_point(int32_t kind, int64_t d, const double* v, const double* y, double lam,

@@ -100,6 +100,8 @@ SIGNATURES = {
     "syscd_apply_dv": (c_i32, [c_i32, c_i64, c_vp, c_vp, c_vp, c_f64, c_f64, c_vp, c_vp]),
     "syscd_grad": (c_i32, [c_i32, c_i64, c_vp, c_vp, c_f64, c_f64, c_vp, c_f64, c_vp, c_vp]),
     "syscd_dual_point": (c_i32, [c_i32, c_i64, c_vp, c_vp, c_f64, c_f64, c_vp, c_vp]),
+    "syscd_node_delta": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_i32, c_vp]),
+    "syscd_vec_add": (c_i32, [c_i64, c_vp, c_vp, c_vp]),
     "syscd_dense_matvec": (c_i32, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "syscd_dense_rmatvec": (c_i32, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "syscd_dense_col_sq_norms": (c_i32, [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),

@@ -57,6 +57,22 @@ __global__ void k_grad(int kind, int64_t d, const double* __restrict__ v, const 
   }
 }
 
+// T2 > 1 node bookkeeping (solvers.py:393,423): acc (+)= v_node - v, v += acc
+__global__ void k_node_delta(int64_t d, const double* __restrict__ v_node,
+                             const double* __restrict__ v, double* __restrict__ acc, int first) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double dv = v_node[i] - v[i];
+    acc[i] = first ? dv : acc[i] + dv;
+  }
+}
+
+__global__ void k_vec_add(int64_t d, double* __restrict__ v, const double* __restrict__ acc) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d;
+       i += (int64_t)gridDim.x * blockDim.x)
+    v[i] += acc[i];
+}
+
 __global__ void k_dual_point(int kind, int64_t d, const double* __restrict__ v,
                              const double* __restrict__ y, double lam, double n,
                              double* __restrict__ w) {
@@ -387,6 +403,27 @@ extern "C" int syscd_grad(int32_t kind, int64_t d, const double* v, const double
   }
   k_grad<<<grid_for(d, 256), 256, 0, (cudaStream_t)stream>>>(kind, d, v, y, lam, n_coords, v_node,
                                                               drift, u);
+  SYSCD_CUDA_TRY(cudaGetLastError());
+  return SYSCD_OK;
+}
+
+extern "C" int syscd_node_delta(int64_t d, const double* v_node, const double* v, double* acc,
+                                int32_t first, void* stream) {
+  if (!v_node || !v || !acc || d < 1) {
+    set_error("syscd_node_delta: invalid arguments");
+    return SYSCD_EINVAL;
+  }
+  k_node_delta<<<grid_for(d, 256), 256, 0, (cudaStream_t)stream>>>(d, v_node, v, acc, first);
+  SYSCD_CUDA_TRY(cudaGetLastError());
+  return SYSCD_OK;
+}
+
+extern "C" int syscd_vec_add(int64_t d, double* v, const double* acc, void* stream) {
+  if (!v || !acc || d < 1) {
+    set_error("syscd_vec_add: invalid arguments");
+    return SYSCD_EINVAL;
+  }
+  k_vec_add<<<grid_for(d, 256), 256, 0, (cudaStream_t)stream>>>(d, v, acc);
   SYSCD_CUDA_TRY(cudaGetLastError());
   return SYSCD_OK;
 }

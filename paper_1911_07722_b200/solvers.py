@@ -426,7 +426,7 @@ class _Engine:
         # inner one: round ids are consumed in increasing order (the plan
         # tables are prefetched in that order) with one v_node per local node.
         drift = cfg.K * dp.gamma
-        delta_sum = torch.zeros(dp.d, dtype=torch.float64, device="cuda")
+        delta_sum = torch.empty(dp.d, dtype=torch.float64, device="cuda")
         u_k = torch.zeros_like(self._u_buf)[:dp.d]
         v_nodes = [self.v.clone() for _ in range(self.K_local)]
         for t2 in range(cfg.T2):
@@ -440,10 +440,11 @@ class _Engine:
                 self.epoch(rid, u_k, k, k + 1)
                 call("syscd_apply_dv", dp.kind, dp.d, _ptr(self.dv), _ptr(v_node), None, dp.lam,
                      dp.n_coords, None, _stream())
-        for v_node in v_nodes:  # ascending node order (reduce_replicas, solvers.py:423)
-            delta_sum += v_node - self.v
+        for k, v_node in enumerate(v_nodes):  # ascending node order (solvers.py:423)
+            call("syscd_node_delta", dp.d, _ptr(v_node), self._p_v, _ptr(delta_sum), int(k == 0),
+                 _stream())
         self.dist.allreduce_(delta_sum)
-        self.v += delta_sum
+        call("syscd_vec_add", dp.d, self._p_v, _ptr(delta_sum), _stream())
         dp.grad_into(self.v, self.u)
 
     def updates_last_round(self, rid):
