@@ -571,9 +571,7 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
               // ---- resolve block c = e - LL (register slot (i + 1) % NSLOT)
               const int c = e - LL;
               const int64_t cpub = ebase + c;
-#ifndef SYSCD_GRID_NOSYNC  // experiment: no grid dependency (wrong results)
               mbar_wait(&totbar[cpub % kGTot], (uint32_t)((cpub / kGTot) & 1));
-#endif
               GSTAMP(3);
               const float* t = tot + (cpub % kGTot) * kGVal;
               float dcur[BB];
