@@ -51,6 +51,10 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // One fp64 Newton step on h itself then polishes the root to the accuracy of
 // the fp32 sigmoid.  Returns false (caller falls back to the bracketed loop)
 // when 8 steps do not converge or the residual of h is not small.
+#ifdef SYSCD_NEWTON_HIST
+// experiment: [tail][iterations] counts and fallbacks of the fast path
+__device__ unsigned long long g_newton_hist[2][12];
+#endif
 __device__ __forceinline__ bool logistic_dual_fast(double lin, double aq, double alpha, double n,
                                                    double* s_out) {
   const double inv_n = 1.0 / n;
@@ -74,8 +78,14 @@ __device__ __forceinline__ bool logistic_dual_fast(double lin, double aq, double
   }
   const float log_aq = __logf(aqf);
   bool conv = false;
+#ifdef SYSCD_NEWTON_HIST
+  int its = 0;
+#endif
 #pragma unroll 1
   for (int it = 0; it < 8; ++it) {
+#ifdef SYSCD_NEWTON_HIST
+    ++its;
+#endif
     const float e = __expf(-fabsf(sp));
     const float w = rcp_approx(1.f + e);
     float ns;
@@ -108,8 +118,11 @@ __device__ __forceinline__ bool logistic_dual_fast(double lin, double aq, double
     // (and the fp64 polish squares it again; its residual check guards the
     // rest): exit one iteration earlier than waiting for a 1e-5 step.  The
     // tail contraction converges linearly and keeps the 1e-5 test.
+#ifndef SYSCD_NEWTON_EXIT
+#define SYSCD_NEWTON_EXIT 4e-3f
+#endif
 #ifndef SYSCD_TAIL_CONTRACTION
-    if (fabsf(step) <= 4e-3f * fmaxf(1.f, fabsf(sp))) {
+    if (fabsf(step) <= SYSCD_NEWTON_EXIT * fmaxf(1.f, fabsf(sp))) {
 #else
     if (fabsf(step) <= (tail ? 1e-5f : 4e-3f) * fmaxf(1.f, fabsf(sp))) {
 #endif
@@ -117,12 +130,20 @@ __device__ __forceinline__ bool logistic_dual_fast(double lin, double aq, double
       break;
     }
   }
+#ifdef SYSCD_NEWTON_HIST
+  atomicAdd(&g_newton_hist[tail ? 1 : 0][conv ? its : 9], 1ull);
+#endif
   const double s = left ? (double)sp : -(double)sp;
   if (!conv || !isfinite(s)) return false;
   const double t = sigmoid_fast(s);
   const double h = lin + aq * (t - alpha) + s * inv_n;
   const double dh = aq * t * (1.0 - t) + inv_n;
-  if (!(fabs(h) <= 1e-4 * dh * fmax(1.0, fabs(s)))) return false;
+  if (!(fabs(h) <= 1e-4 * dh * fmax(1.0, fabs(s)))) {
+#ifdef SYSCD_NEWTON_HIST
+    atomicAdd(&g_newton_hist[tail ? 1 : 0][10], 1ull);
+#endif
+    return false;
+  }
   *s_out = s - h * (double)rcp_approx((float)dh);
   return true;
 }

@@ -775,3 +775,13 @@ extern "C" int syscd_sparse_epoch(const syscd_sparse_epoch_args* e, void* stream
   }
   return SYSCD_OK;
 }
+
+#ifdef SYSCD_NEWTON_HIST
+// experiment hook: copy out (and reset) the fast-path iteration histogram
+extern "C" int syscd_debug_newton_hist(unsigned long long* out24) {
+  cudaMemcpyFromSymbol(out24, syscd::g_newton_hist, sizeof(unsigned long long) * 24);
+  unsigned long long z[24] = {0};
+  cudaMemcpyToSymbol(syscd::g_newton_hist, z, sizeof(z));
+  return 0;
+}
+#endif
