@@ -52,6 +52,9 @@ constexpr int kGRed = 8;      // CTA-reduction slots (events)
 #ifndef SYSCD_GRID_CHAINS
 #define SYSCD_GRID_CHAINS 1  // accumulator chains per partial value
 #endif
+#ifndef SYSCD_GRID_TSUM
+#define SYSCD_GRID_TSUM 1  // reducer: all totals in one shuffle-transposed warp sum
+#endif
 #ifndef SYSCD_GRID_SLEEP
 #define SYSCD_GRID_SLEEP 256  // reducer poll back-off (ns)
 #endif
@@ -245,6 +248,13 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
   // does not cover the other threads' writes
   fence_proxy_async();
   for (int i = tid; i < 16 * kGRecent; i += blockDim.x) recent[i] = make_int2(-1, 0);
+#if defined(SYSCD_TRACE) && defined(SYSCD_TRACE_LIGHT)
+  if (A.dbg && tid == 0) {  // SM of every CTA (scripts/grid_skew.py)
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    A.dbg[8192 + 2 * 1024 * 160 + cta] = smid;
+  }
+#endif
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
@@ -294,6 +304,27 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
         for (int q = 0; q < NQ; ++q) ok &= (uint32_t)(wv[k][c][q] >> 32) == tag;
       if (!__all_sync(0xffffffffu, ok)) continue;
       float* t = tot + (r % kGTot) * kGVal;
+#if SYSCD_GRID_TSUM
+      // the NS totals in one shuffle-transposed reduction (NP-1 + 5-log2 NP
+      // shuffles instead of 5 NS): the hand-over is on the grid's critical
+      // path (last publication -> totals -> next resolve)
+      {
+        float pv[NP];
+#pragma unroll
+        for (int c = 0; c < NP; ++c) {
+          float acc = 0.f;
+          if (c < NS) {
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) acc += __uint_as_float((uint32_t)wv[k][c][q]);
+          }
+          pv[c] = acc;
+        }
+        const float tv = warp_sum_multi<NP>(pv, lane);
+        const int idx = multi_index<NP>(lane);
+        if ((lane & (32 / NP - 1)) == 0 && idx < NS) t[idx] = tv;
+      }
+      __syncwarp();
+#else
 #pragma unroll
       for (int c = 0; c < NS; ++c) {
         float acc = 0.f;
@@ -302,6 +333,7 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
         acc = warp_sum(acc);
         if (lane == 0) t[c] = acc;
       }
+#endif
       if (lane == 0) {
 #ifdef SYSCD_TRACE
 #ifndef SYSCD_TRACE_LIGHT

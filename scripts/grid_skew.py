@@ -42,3 +42,8 @@ vals, cnts = np.unique(lastc, return_counts=True)
 top = np.argsort(cnts)[::-1][:10]
 print("CTA most often last:", [(int(vals[i]), int(cnts[i])) for i in top])
 np.savez_compressed("gpurun_out/grid_skew.npz", pubt=pubt, tott=tott)
+smid = allb[8192 + 2 * 1024 * 160:8192 + 2 * 1024 * 160 + G].astype(int)
+print("CTA -> SM:", smid.tolist())
+print("slowest CTAs' SMs:", [(int(c), int(smid[c]), int(ml[c])) for c in order[:16]])
+print("lag by SM id (sorted by SM):", [(int(smid[c]), int(ml[c])) for c in np.argsort(smid)])
+np.savez_compressed("gpurun_out/grid_skew_sm.npz", smid=smid, lag=ml)
