@@ -320,8 +320,13 @@ def _epoch_kernel_name(dp, eng):
     from paper_1911_07722_b200._lib import lib
     if dp.storage != "dense":
         return "k_sparse_epoch"
-    return lib().syscd_dense_epoch_kernel(dp.d, dp.lda, eng.n_parts_local, eng.max_pu,
-                                          eng.bucket_cols).decode()
+    if dp.d <= 32:
+        return "k_small_epoch"
+    if dp.d <= 16 * 1280:  # csrc/epoch_mid.cu kMidMaxD
+        return "k_mid_epoch"
+    if int(lib().syscd_dense_epoch_workspace_bytes(dp.d, eng.n_parts_local)) > 0:
+        return "k_grid_epoch"
+    return "k_dense_epoch"
 
 
 def dual_suboptimality(pb, solver, res, k, target, epochs=150, dist=None):

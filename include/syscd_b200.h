@@ -101,8 +101,6 @@ typedef struct {
 int64_t syscd_plan_workspace_bytes(const syscd_plan_desc* desc, int32_t n_rounds);
 /* upper bound of the per-round update count (size seq_stride >= this) */
 int64_t syscd_plan_max_updates(const syscd_plan_desc* desc);
-/* upper bound of any one partition's updates in a round */
-int64_t syscd_plan_max_part_updates(const syscd_plan_desc* desc);
 int syscd_plan(const syscd_plan_desc* desc, int64_t rid0, int32_t n_rounds, int32_t* seq,
                int64_t seq_stride, int64_t* work_prefix, void* workspace, int64_t workspace_bytes,
                void* stream);
@@ -137,26 +135,10 @@ typedef struct {
   int32_t* status;         /* device int, OR-ed with 2 on a non-finite step         */
   void* workspace;         /* device scratch, >= syscd_dense_epoch_workspace_bytes   */
   int64_t workspace_bytes;
-  int32_t max_part_updates; /* bound on any one partition's updates in this round
-                              (syscd_plan_max_part_updates); 0 = unknown. Rounds of
-                              short partitions (<= 16) on tall columns run the
-                              partition-Gram kernel, which writes ONE partials row */
-  int32_t bucket_cols;      /* > 0: every partition's updates this round are whole
-                              buckets of bucket_cols consecutive store columns
-                              (bucket b = columns [b*bucket_cols, (b+1)*bucket_cols),
-                              no repeats): enables the partition-Gram kernel     */
 } syscd_dense_epoch_args;
 
 /* workers the dense epoch uses for this geometry (partials must hold that many rows) */
 int syscd_dense_epoch_workers(int64_t d, int32_t n_parts, int32_t* n_workers, int32_t* cluster);
-/* name of the epoch kernel syscd_dense_epoch runs for this geometry and round
- * shape (max_part_updates / bucket_cols as in syscd_dense_epoch_args) */
-const char* syscd_dense_epoch_kernel(int64_t d, int64_t lda, int32_t n_parts,
-                                     int32_t max_part_updates, int32_t bucket_cols);
-/* syscd_dense_epoch_workers for that round shape (the partition-Gram kernel
- * writes one partials row) */
-int syscd_dense_epoch_workers2(int64_t d, int64_t lda, int32_t n_parts, int32_t max_part_updates,
-                               int32_t bucket_cols, int32_t* n_workers, int32_t* cluster);
 /* device scratch the epoch needs for this geometry (0 for the cluster kernel;
  * the grid-wide kernel used for very tall columns needs its reduction slots) */
 int64_t syscd_dense_epoch_workspace_bytes(int64_t d, int32_t n_parts);

@@ -40,7 +40,7 @@ class DenseEpochArgs(ctypes.Structure):
         ("alpha", c_vp), ("u", c_vp), ("seq", c_vp), ("work_prefix", c_vp), ("n_parts", c_i32),
         ("a", c_f64), ("lam", c_f64), ("n_coords", c_f64), ("iid", c_i32), ("n_store", c_i64),
         ("partials", c_vp), ("part_ld", c_i64), ("status", c_vp), ("workspace", c_vp),
-        ("workspace_bytes", c_i64), ("max_part_updates", c_i32), ("bucket_cols", c_i32),
+        ("workspace_bytes", c_i64),
     ]
 
 
@@ -87,14 +87,10 @@ SIGNATURES = {
     "syscd_rng_integers": (c_i32, [c_u64, ctypes.POINTER(c_u64), c_i32, c_i64, c_i64, c_i64, c_vp]),
     "syscd_plan_workspace_bytes": (c_i64, [ctypes.POINTER(PlanDesc), c_i32]),
     "syscd_plan_max_updates": (c_i64, [ctypes.POINTER(PlanDesc)]),
-    "syscd_plan_max_part_updates": (c_i64, [ctypes.POINTER(PlanDesc)]),
     "syscd_plan": (c_i32, [ctypes.POINTER(PlanDesc), c_i64, c_i32, c_vp, c_i64, c_vp, c_vp, c_i64,
                            c_vp]),
     "syscd_dense_epoch_workers": (c_i32, [c_i64, c_i32, ctypes.POINTER(c_i32),
                                           ctypes.POINTER(c_i32)]),
-    "syscd_dense_epoch_kernel": (ctypes.c_char_p, [c_i64, c_i64, c_i32, c_i32, c_i32]),
-    "syscd_dense_epoch_workers2": (c_i32, [c_i64, c_i64, c_i32, c_i32, c_i32,
-                                           ctypes.POINTER(c_i32), ctypes.POINTER(c_i32)]),
     "syscd_dense_epoch_workspace_bytes": (c_i64, [c_i64, c_i32]),
     "syscd_dense_epoch": (c_i32, [ctypes.POINTER(DenseEpochArgs), c_vp]),
     "syscd_sparse_epoch_workers": (c_i32, [c_i64, c_i32, ctypes.POINTER(c_i32)]),

@@ -15,7 +15,7 @@ ROOT = os.path.dirname(PKG)
 TRACE = bool(os.environ.get("SYSCD_TRACE"))
 LIB = os.path.join(PKG, "libsyscd_b200_trace.so" if TRACE else
                    os.environ.get("SYSCD_LIB_NAME", "libsyscd_b200.so"))
-SOURCES = ["capi.cu", "plan.cu", "epoch_dense.cu", "epoch_grid.cu", "epoch_pgram.cu", "epoch_small.cu", "epoch_mid.cu", "epoch_sparse.cu", "exact_logistic.cu", "vecops.cu", "libsvm_io.cu", "epoch_wild.cu", "datagen.cu"]
+SOURCES = ["capi.cu", "plan.cu", "epoch_dense.cu", "epoch_grid.cu", "epoch_small.cu", "epoch_mid.cu", "epoch_sparse.cu", "exact_logistic.cu", "vecops.cu", "libsvm_io.cu", "epoch_wild.cu", "datagen.cu"]
 HEADERS = ["common.cuh", "rng.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

@@ -571,17 +571,6 @@ constexpr int64_t kSmallMaxD = 32;
 int64_t grid_workspace_bytes(int G);
 int grid_launch(const syscd_dense_epoch_args* e, void* workspace, int64_t ws_bytes,
                 cudaStream_t stream);
-bool pgram_applicable(int64_t d, int32_t n_parts, int32_t max_part_updates, int32_t bucket_cols,
-                      int64_t lda);
-int64_t pgram_workspace_bytes(int64_t d);
-int pgram_launch(const syscd_dense_epoch_args* e, cudaStream_t stream);
-// partition-Gram kernel for short partitions of tall columns (SYSCD_PGRAM=0 disables)
-static bool use_pgram(int64_t d, int32_t n_parts, int32_t max_part_updates, int32_t bucket_cols,
-                      int64_t lda) {
-  const char* env = getenv("SYSCD_PGRAM");
-  if (env && *env == '0') return false;
-  return pgram_applicable(d, n_parts, max_part_updates, bucket_cols, lda);
-}
 
 static int choose(int64_t d, int32_t n_parts, Choice* out) {
   std::lock_guard<std::mutex> lock(g_table_mu);
@@ -648,30 +637,6 @@ static void* g_dbg_buffer = nullptr;
 // and flush done).
 extern "C" void syscd_debug_set_timeline(void* device_buffer) { g_dbg_buffer = device_buffer; }
 
-extern "C" const char* syscd_dense_epoch_kernel(int64_t d, int64_t lda, int32_t n_parts,
-                                                 int32_t max_part_updates, int32_t bucket_cols) {
-  if (d < 1 || n_parts < 1) return "";
-  if (d <= kSmallMaxD) return "k_small_epoch";
-  if (mid_applicable(d, n_parts, nullptr, nullptr)) return "k_mid_epoch";
-  if (use_pgram(d, n_parts, max_part_updates, bucket_cols, lda)) return "k_pgram_epoch";
-  Choice ch;
-  if (choose(d, n_parts, &ch) != SYSCD_OK) return "";
-  return ch.grid ? "k_grid_epoch" : "k_dense_epoch";
-}
-
-extern "C" int syscd_dense_epoch_workers2(int64_t d, int64_t lda, int32_t n_parts,
-                                          int32_t max_part_updates, int32_t bucket_cols,
-                                          int32_t* n_workers, int32_t* cluster) {
-  if (d > kSmallMaxD && n_parts >= 1 && n_workers &&
-      !mid_applicable(d, n_parts, nullptr, nullptr) &&
-      use_pgram(d, n_parts, max_part_updates, bucket_cols, lda)) {
-    *n_workers = 1;  // one partials row: sum_p dv_p
-    if (cluster) *cluster = 0;
-    return SYSCD_OK;
-  }
-  return syscd_dense_epoch_workers(d, n_parts, n_workers, cluster);
-}
-
 extern "C" int syscd_dense_epoch_workers(int64_t d, int32_t n_parts, int32_t* n_workers,
                                          int32_t* cluster) {
   if (d < 1 || n_parts < 1 || !n_workers) {
@@ -702,14 +667,11 @@ extern "C" int64_t syscd_dense_epoch_workspace_bytes(int64_t d, int32_t n_parts)
   if (n_parts >= 1 && mid_applicable(d, n_parts, nullptr, nullptr)) return 0;
   Choice ch;
   if (d < 1 || n_parts < 1 || choose(d, n_parts, &ch) != SYSCD_OK) return -1;
-  // the partition-Gram kernel's slots, whenever a round of short partitions
-  // could select it (the partition bound is a per-round argument)
-  const int64_t pg = use_pgram(d, n_parts, 8, 8, 32) ? pgram_workspace_bytes(d) : 0;
-  if (!ch.grid) return pg;
+  if (!ch.grid) return 0;
   int idx, G, st;
   size_t sm;
   grid_choose(d, &idx, &G, &st, &sm, nullptr);
-  return std::max(pg, grid_workspace_bytes(G));
+  return grid_workspace_bytes(G);
 }
 
 extern "C" int syscd_dense_epoch(const syscd_dense_epoch_args* e, void* stream) {
@@ -736,13 +698,6 @@ extern "C" int syscd_dense_epoch(const syscd_dense_epoch_args* e, void* stream) 
       return SYSCD_EINVAL;
     }
     return mid_launch(e, (cudaStream_t)stream);
-  }
-  if (use_pgram(e->d, e->n_parts, e->max_part_updates, e->bucket_cols, e->lda)) {
-    if (e->part_ld < e->d) {
-      set_error("syscd_dense_epoch: part_ld < d");
-      return SYSCD_EINVAL;
-    }
-    return pgram_launch(e, (cudaStream_t)stream);
   }
   Choice ch;
   int st = choose(e->d, e->n_parts, &ch);

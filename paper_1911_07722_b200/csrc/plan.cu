@@ -15,8 +15,6 @@
 //                    (solvers.py:326-333)
 // Rounds are independent, so a batch of rounds is planned in one pass (the
 // permutations are data-independent and can run ahead on a side stream).
-#include <algorithm>
-
 #include <cub/block/block_scan.cuh>
 
 #include "common.cuh"
@@ -278,25 +276,6 @@ extern "C" int64_t syscd_plan_max_updates(const syscd_plan_desc* d) {
     }
   }
   return total;
-}
-
-extern "C" int64_t syscd_plan_max_part_updates(const syscd_plan_desc* d) {
-  if (plan_check(d) != SYSCD_OK) return -1;
-  int64_t best = 0;
-  for (int k = 0; k < d->n_nodes_local; ++k) {
-    const int64_t nb = d->node_bucket_ptr[k + 1] - d->node_bucket_ptr[k];
-    const int64_t cnt = (nb + d->P - 1) / d->P;  // partition 0 holds the most buckets
-    int64_t t3, t4;
-    if (d->sampling == 0) {
-      t3 = d->T3 < 0 ? cnt : std::min<int64_t>(d->T3, cnt);
-      t4 = d->T4 < 0 ? d->bucket_size : std::min<int64_t>(d->T4, d->bucket_size);
-    } else {
-      t3 = d->T3 < 0 ? cnt : d->T3;
-      t4 = d->T4 < 0 ? d->bucket_size : d->T4;
-    }
-    best = std::max(best, t3 * t4);
-  }
-  return best;
 }
 
 extern "C" int syscd_plan(const syscd_plan_desc* d, int64_t rid0, int32_t n_rounds, int32_t* seq,

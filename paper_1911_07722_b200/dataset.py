@@ -23,11 +23,7 @@ COORDINATES_ARE_EXAMPLES = "coordinates_are_examples"
 
 
 def padded_ld(d):
-    """Leading dimension of a dense store: 16-byte column starts (1-D bulk
-    copies); tall stores (d >= 4096) start every column on 128 bytes so the
-    partition-Gram epoch can move bucket tiles with one 3-D tensor copy."""
-    q = 32 if int(d) >= 4096 else 4
-    return (int(d) + q - 1) // q * q
+    return (int(d) + 3) // 4 * 4
 
 
 class ColumnMatrix:

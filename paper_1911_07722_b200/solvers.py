@@ -191,17 +191,6 @@ class _Engine:
         self.stride = int(L.syscd_plan_max_updates(ctypes.byref(self.desc)))
         if self.stride < 0:
             call("syscd_plan_max_updates")
-        # bound on one partition's updates per round (selects the dense kernel)
-        self.max_pu = int(L.syscd_plan_max_part_updates(ctypes.byref(self.desc)))
-        if self.max_pu < 0:
-            call("syscd_plan_max_part_updates")
-        # rounds of whole buckets of B consecutive store columns (perm sampling,
-        # every coordinate of a bucket, every bucket starting at a multiple of
-        # B in the store, so column j lies in the bucket starting at j - j % B):
-        # the partition-Gram kernel can stage a bucket as one tile
-        whole = cfg.sampling == "perm" and (cfg.T4 is None or cfg.T4 >= B)
-        laid = bool(np.all(np.asarray(store_col, dtype=np.int64) % B == 0))
-        self.bucket_cols = int(B) if whole and laid else 0
         self.R = max(1, min(cfg.plan_batch, cfg.n_rounds * cfg.T2 if cfg.n_rounds else 1))
         # per-round update counts, written by the planner (round_updates[rid]);
         # sized for every round plus the batch planned ahead of the last one
@@ -273,16 +262,14 @@ class _Engine:
             e.status = self.status.data_ptr()
             e.workspace = self.epoch_ws.data_ptr()
             e.workspace_bytes = self.epoch_ws.numel()
-            e.max_part_updates = self.max_pu
-            e.bucket_cols = self.bucket_cols
             self._dargs = e
             self._dargs_ref = ctypes.byref(e)
 
-    def _dense_workers(self, d, n_parts):
+    @staticmethod
+    def _dense_workers(d, n_parts):
         nw = ctypes.c_int32(0)
         cl = ctypes.c_int32(0)
-        call("syscd_dense_epoch_workers2", d, self.dp.lda, n_parts, self.max_pu,
-             self.bucket_cols, ctypes.byref(nw), ctypes.byref(cl))
+        call("syscd_dense_epoch_workers", d, n_parts, ctypes.byref(nw), ctypes.byref(cl))
         return nw.value, cl.value
 
     # -- one device round (rid) over node range [k0, k1) with lin_vec u -------
