@@ -56,8 +56,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
 __device__ unsigned long long g_newton_hist[2][12];
 #endif
 __device__ __forceinline__ bool logistic_dual_fast(double lin, double aq, double alpha, double n,
-                                                   double* s_out) {
-  const double inv_n = 1.0 / n;
+                                                   double inv_n, double* s_out, double* alpha_out) {
   const double C = aq * alpha - lin;
   const bool left = 0.5 * aq - C > 0.0;
   const double Cl = left ? C : aq - C;
@@ -144,7 +143,12 @@ __device__ __forceinline__ bool logistic_dual_fast(double lin, double aq, double
 #endif
     return false;
   }
-  *s_out = s - h * (double)rcp_approx((float)dh);
+  const double ds = -h * (double)rcp_approx((float)dh);
+  *s_out = s + ds;
+  // sigma(s + ds) to first order: the polish step is ~1e-5 (the fp32 loop's
+  // exit), so the dropped t (1-t)(1-2t) ds^2 / 2 is below fp32 resolution,
+  // and no second sigmoid evaluation sits on the chain
+  *alpha_out = t + t * (1.0 - t) * ds;
   return true;
 }
 
@@ -155,11 +159,12 @@ __device__ __forceinline__ bool logistic_dual_fast(double lin, double aq, double
 // logit evaluated by fp32 SFU intrinsics.  The result is stored as fp32
 // alpha = sigma(s) and sigma' <= 1/4, so the iteration stops at
 // |ds| <= 1e-9 max(1,|s|) (the oracle uses 1e-13 with fp64 transcendentals).
+// inv_n = 1/n precomputed by the caller (a loop-invariant fp64 division the
+// chain should not carry)
 __device__ __forceinline__ double logistic_dual_solve(double lin, double aq, double alpha,
-                                                      double n) {
-  double s = 0.0;
-  if (aq > 0.0 && logistic_dual_fast(lin, aq, alpha, n, &s)) return sigmoid_fast(s);
-  const double inv_n = 1.0 / n;
+                                                      double n, double inv_n) {
+  double s = 0.0, an = 0.0;
+  if (aq > 0.0 && logistic_dual_fast(lin, aq, alpha, n, inv_n, &s, &an)) return an;
   double lo = -n * (lin + aq * (1.0 - alpha)) - 1.0;
   double hi = n * (aq * alpha - lin) + 1.0;
   s = 0.0;
@@ -208,7 +213,7 @@ __device__ __forceinline__ double coord_step(int kind, double lin, double a, dou
       return fmin(fmax(z, 0.0), 1.0);
     }
     default:  // SYSCD_LOGISTIC_DUAL
-      return logistic_dual_solve(lin, a * q, alpha, n);
+      return logistic_dual_solve(lin, a * q, alpha, n, 1.0 / n);
   }
 }
 

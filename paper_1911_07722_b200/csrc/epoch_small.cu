@@ -63,7 +63,8 @@ __device__ __forceinline__ float small_step(float r, float alpha, float q, float
     const float z = alpha - (r - inv_n) * inv_aq;
     return q > 0.f ? fminf(fmaxf(z, 0.f), 1.f) : 1.f;
   } else {
-    return (float)logistic_dual_solve((double)r, A.a_d * (double)q, (double)alpha, A.n_coords);
+    return (float)logistic_dual_solve((double)r, A.a_d * (double)q, (double)alpha, A.n_coords,
+                                      1.0 / A.n_coords);
   }
 }
 

@@ -58,7 +58,7 @@ struct SparseArgs {
   int32_t n_parts;
   float a;
   float lam_f, inv_n_f;
-  double a_d, lam, n_coords;
+  double a_d, lam, n_coords, inv_n_d;
   int32_t kind, iid;
   unsigned long long* dv_work;  // tagged replicas (see syscd_b200.h)
   float* delta_v;
@@ -92,7 +92,8 @@ __device__ __forceinline__ void rep_store(unsigned long long* dv, int64_t r, uin
 template <int KIND>
 __device__ __forceinline__ float sparse_step(const SparseArgs& A, float lin, float aj, float qj) {
   if (KIND == SYSCD_LOGISTIC_DUAL)
-    return (float)logistic_dual_solve((double)lin, A.a_d * (double)qj, (double)aj, A.n_coords);
+    return (float)logistic_dual_solve((double)lin, A.a_d * (double)qj, (double)aj, A.n_coords,
+                                      A.inv_n_d);
   return coord_step_f(KIND, lin, A.a, qj, A.lam_f, aj, A.inv_n_f);
 }
 
@@ -743,6 +744,7 @@ extern "C" int syscd_sparse_epoch(const syscd_sparse_epoch_args* e, void* stream
   A.inv_n_f = (float)(1.0 / e->n_coords);
   A.lam = e->lam;
   A.n_coords = e->n_coords;
+  A.inv_n_d = 1.0 / e->n_coords;
   A.kind = e->kind;
   A.iid = e->iid;
   A.dv_work = (unsigned long long*)e->dv_work;
