@@ -109,6 +109,12 @@ CASES = [
     (4, 0.0002, dict(K=1, P=4, bucket_size=8, T1=3)),
     (4, 0.0002, dict(K=2, P=3, bucket_size=16, sampling="iid", T3=3, T4=4, T1=2)),
     (4, 0.0002, dict(K=1, P=1, bucket_size=8, T1=2)),
+    # d >= 4096: every chain of a T2 = 1 round at once, each by a team of
+    # threads (round_teams / team_chain in oracle/syscd_cpu.cpp)
+    (2, 0.02, dict(K=1, P=4, bucket_size=2, T1=3)),
+    (2, 0.02, dict(K=2, P=3, bucket_size=2, T1=3)),
+    (0, 0.25, dict(K=2, P=2, bucket_size=4, T1=3)),
+    (3, 0.005, dict(K=3, P=1, bucket_size=8, T1=2)),
 ]
 
 
@@ -124,7 +130,8 @@ def test_matches_python_oracle(cfg_id, scale, kw):
 def test_thread_count_independent():
     for cfg_id, scale, kw in [(0, 0.05, dict(K=1, P=4, bucket_size=4, T1=3)),
                               (4, 0.0002, dict(K=1, P=4, bucket_size=8, T1=2)),
-                              (3, 0.002, dict(K=1, P=1, bucket_size=8, T1=2))]:
+                              (3, 0.002, dict(K=1, P=1, bucket_size=8, T1=2)),
+                              (2, 0.02, dict(K=2, P=3, bucket_size=2, T1=2))]:
         spec = _spec_from_oracle(oracle_problem(cfg_id, scale))
         cfg = O.OracleConfig(**kw)
         r1 = C.run_syscd(spec, cfg, threads=1)
