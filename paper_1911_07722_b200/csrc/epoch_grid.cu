@@ -367,7 +367,11 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
     // producer state (warp NWC)
     int64_t valid = d - row0;
     valid = valid < 0 ? 0 : (valid > cta_rows ? cta_rows : valid);
+#ifdef SYSCD_GRID_NODATA  // experiment: the event chain without the A stream (wrong results)
+    const uint32_t bytes = 0;
+#else
     const uint32_t bytes = (uint32_t)(((valid + 3) / 4) * 16);
+#endif
     const uint64_t policy = A.evict_first ? policy_evict_first() : policy_evict_last();
     uint32_t stage = 0, phase = 0;
     // coordinate ids, alpha and q of 32 columns at a time (lane-parallel), so

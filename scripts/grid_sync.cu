@@ -1,0 +1,183 @@
+// Micro-benchmark: the cost of the grid epoch's cross-CTA exchange alone.
+// G CTAs (one per SM) run E events; in event e every CTA publishes one
+// tagged 64-bit word per value (NS values, CTA-major records as in
+// k_grid_epoch) and must have seen every CTA's words of event e - L before it
+// publishes event e + 1 (lookahead L).  One warp per CTA publishes (lane <
+// NS), another polls (each lane gathers 5 CTAs' records) and hands the
+// completed event to the publisher through shared memory.  No data, no math:
+// the per-event time is the exchange chain / (L + 1).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/grid_sync scripts/grid_sync.cu
+//   /tmp/grid_sync
+#include <cstdio>
+#include <cstdint>
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+constexpr int NS = 4;
+constexpr int NQ = 5;
+constexpr int NB = 16;  // record slots (events)
+
+__device__ __forceinline__ void st_rel(unsigned long long* p, unsigned long long w) {
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_rel(const unsigned long long* p) {
+  unsigned long long w;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+  return w;
+}
+
+template <int MODE>
+__global__ void k_sync(unsigned long long* recs, int E, int L, int sleep_ns, unsigned long long* t_out) {
+  __shared__ volatile int done;  // events whose totals this CTA has (handed over by the poller)
+  __shared__ volatile int fin[NB];  // fin[r % NB] = r + 1 once event r is complete here
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x, cta = blockIdx.x;
+  if (threadIdx.x == 0) done = 0;
+  if (threadIdx.x < NB) fin[threadIdx.x] = 0;
+  __syncthreads();
+  unsigned long long t0 = 0;
+  if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  if (warp == 0) {
+    // publisher: event e needs the totals of e - L - 1
+    for (int e = 0; e < E; ++e) {
+      if (lane == 0 && e - L - 1 >= 0)
+        while (fin[(e - L - 1) % NB] != e - L) {
+        }
+      __syncwarp();
+      if (lane < NS) {
+        const unsigned long long w = ((unsigned long long)(e + 1) << 32) | (unsigned)(cta + lane);
+        st_rel(recs + ((size_t)(e % NB) * G + cta) * NS + lane, w);
+      }
+    }
+  } else if (MODE == 1) {
+    // k_grid_epoch's reducer: two slots (even / odd events), each pass issues
+    // a slot's missing words, waits for them and checks, then the other slot
+    unsigned long long wv[2][NS][NQ];
+    for (int k = 0; k < 2; ++k)
+      for (int c = 0; c < NS; ++c)
+        for (int q = 0; q < NQ; ++q) wv[k][c][q] = 0ull;
+    int rs[2] = {0, 1};
+    while (rs[0] < E || rs[1] < E) {
+      bool prog = false;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int r = rs[k];
+        if (r >= E) continue;
+        const unsigned long long* rec = recs + (size_t)(r % NB) * G * NS;
+        const unsigned tag = (unsigned)(r + 1);
+#pragma unroll
+        for (int c = 0; c < NS; ++c)
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+            const int cc = lane + 32 * q;
+            if ((unsigned)(wv[k][c][q] >> 32) != tag)
+              wv[k][c][q] = cc < G ? ld_rel(rec + (size_t)cc * NS + c) : ((unsigned long long)tag << 32);
+          }
+        bool ok = true;
+#pragma unroll
+        for (int c = 0; c < NS; ++c)
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) ok &= (unsigned)(wv[k][c][q] >> 32) == tag;
+        if (!__all_sync(0xffffffffu, ok)) continue;
+        if (lane == 0) fin[r % NB] = r + 1;
+        __syncwarp();
+        rs[k] = r + 2;
+        prog = true;
+      }
+      if (!prog && sleep_ns > 0) __nanosleep(sleep_ns);
+    }
+  } else {
+    // poller: D events in flight (issue every in-flight event's missing
+    // words, then hand over the completed ones in order)
+    constexpr int D = MODE == 0 ? 1 : MODE;
+    unsigned long long wv[D][NS][NQ];
+    for (int k = 0; k < D; ++k)
+      for (int c = 0; c < NS; ++c)
+        for (int q = 0; q < NQ; ++q) wv[k][c][q] = 0ull;
+    int r0 = 0;  // oldest event not yet handed over; slot of event r: r % D
+    while (r0 < E) {
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const int r = r0 + ((k - r0 % D + D) % D);
+        if (r >= E) continue;
+        const unsigned long long* rec = recs + (size_t)(r % NB) * G * NS;
+        const unsigned tag = (unsigned)(r + 1);
+#pragma unroll
+        for (int c = 0; c < NS; ++c)
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+            const int cc = lane + 32 * q;
+            if ((unsigned)(wv[k][c][q] >> 32) != tag)
+              wv[k][c][q] = cc < G ? ld_rel(rec + (size_t)cc * NS + c) : ((unsigned long long)tag << 32);
+          }
+      }
+      bool prog = false;
+      for (;;) {
+        const int k = r0 % D;
+        const unsigned tag = (unsigned)(r0 + 1);
+        bool ok = r0 < E;
+#pragma unroll
+        for (int kk = 0; kk < D; ++kk)
+          if (kk == k)
+#pragma unroll
+            for (int c = 0; c < NS; ++c)
+#pragma unroll
+              for (int q = 0; q < NQ; ++q) ok &= (unsigned)(wv[kk][c][q] >> 32) == tag;
+        if (!__all_sync(0xffffffffu, ok)) break;
+        __syncwarp();
+        if (lane == 0) fin[r0 % NB] = r0 + 1;
+        ++r0;
+        prog = true;
+      }
+      if (!prog && sleep_ns > 0) __nanosleep(sleep_ns);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    t_out[cta] = t1 - t0;
+  }
+}
+
+int main(int argc, char** argv) {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int E = 20000;
+  unsigned long long *recs, *tout;
+  cudaMalloc(&recs, (size_t)NB * 160 * NS * 8);
+  cudaMalloc(&tout, 160 * 8);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int Gs[] = {145};
+  const int Ls[] = {2, 3};
+  const int sleeps[] = {0, 256};
+  printf("mode(events in flight) G L sleep_ns us_per_event\n");
+  for (int mode : {0, 1, 2})
+  for (int G : Gs) {
+    if (G > sms) continue;
+    for (int L : Ls)
+      for (int sl : sleeps) {
+        cudaMemset(recs, 0, (size_t)NB * 160 * NS * 8);
+        void* args[] = {&recs, (void*)&E, (void*)&L, (void*)&sl, &tout};
+        int Ev = E;
+        args[1] = &Ev;
+        int Lv = L, slv = sl;
+        args[2] = &Lv;
+        args[3] = &slv;
+        cudaEventRecord(a);
+        void* fn = mode == 0 ? (void*)k_sync<0> : mode == 1 ? (void*)k_sync<1>
+                 : mode == 2 ? (void*)k_sync<2> : (void*)k_sync<3>;
+        cudaLaunchCooperativeKernel(fn, dim3(G), dim3(64), args, 0, 0);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        printf("%d %d %d %d %.3f\n", mode, G, L, sl, ms * 1e3 / E);
+        fflush(stdout);
+      }
+  }
+  printf("status: %s\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
