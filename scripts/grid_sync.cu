@@ -5,7 +5,10 @@
 // publishes event e + 1 (lookahead L).  One warp per CTA publishes (lane <
 // NS), another polls (each lane gathers 5 CTAs' records) and hands the
 // completed event to the publisher through shared memory.  No data, no math:
-// the per-event time is the exchange chain / (L + 1).
+// the per-event time is the exchange chain / (L + 1).  Pollers: MODE 0 one
+// event at a time; 1 k_grid_epoch's two-slot sequential poller; 2 two events
+// in flight, both issued per pass; 4 leader protocol (CTA 0 gathers and
+// broadcasts one word per event).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/grid_sync scripts/grid_sync.cu
 //   /tmp/grid_sync
 #include <cstdio>
@@ -47,6 +50,52 @@ __global__ void k_sync(unsigned long long* recs, int E, int L, int sleep_ns, uns
       if (lane < NS) {
         const unsigned long long w = ((unsigned long long)(e + 1) << 32) | (unsigned)(cta + lane);
         st_rel(recs + ((size_t)(e % NB) * G + cta) * NS + lane, w);
+      }
+    }
+  } else if (MODE == 4) {
+    // leader protocol: CTA 0 gathers every record of event r and publishes one
+    // tagged word (the step); the other CTAs poll only that word
+    unsigned long long* dword = recs + (size_t)NB * 160 * NS;  // [NB] leader words
+    if (cta == 0) {
+      unsigned long long wv[NS][NQ];
+      for (int c = 0; c < NS; ++c)
+        for (int q = 0; q < NQ; ++q) wv[c][q] = 0ull;
+      for (int r = 0; r < E; ++r) {
+        const unsigned long long* rec = recs + (size_t)(r % NB) * G * NS;
+        const unsigned tag = (unsigned)(r + 1);
+        for (;;) {
+          bool ok = true;
+#pragma unroll
+          for (int c = 0; c < NS; ++c)
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+              const int cc = lane + 32 * q;
+              if ((unsigned)(wv[c][q] >> 32) != tag)
+                wv[c][q] = cc < G ? ld_rel(rec + (size_t)cc * NS + c) : ((unsigned long long)tag << 32);
+            }
+#pragma unroll
+          for (int c = 0; c < NS; ++c)
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) ok &= (unsigned)(wv[c][q] >> 32) == tag;
+          if (__all_sync(0xffffffffu, ok)) break;
+          if (sleep_ns > 0) __nanosleep(sleep_ns);
+        }
+        if (lane == 0) {
+          st_rel(dword + (r % NB), ((unsigned long long)tag << 32) | 7u);
+          fin[r % NB] = r + 1;
+        }
+        __syncwarp();
+      }
+    } else {
+      for (int r = 0; r < E; ++r) {
+        const unsigned tag = (unsigned)(r + 1);
+        if (lane == 0) {
+          while ((unsigned)(ld_rel(dword + (r % NB)) >> 32) != tag) {
+            if (sleep_ns > 0) __nanosleep(sleep_ns);
+          }
+          fin[r % NB] = r + 1;
+        }
+        __syncwarp();
       }
     }
   } else if (MODE == 1) {
@@ -145,21 +194,21 @@ int main(int argc, char** argv) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int E = 20000;
   unsigned long long *recs, *tout;
-  cudaMalloc(&recs, (size_t)NB * 160 * NS * 8);
+  cudaMalloc(&recs, ((size_t)NB * 160 * NS + NB) * 8);
   cudaMalloc(&tout, 160 * 8);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   const int Gs[] = {145};
-  const int Ls[] = {2, 3};
+  const int Ls[] = {1, 2, 3};
   const int sleeps[] = {0, 256};
   printf("mode(events in flight) G L sleep_ns us_per_event\n");
-  for (int mode : {0, 1, 2})
+  for (int mode : {1, 2, 4})
   for (int G : Gs) {
     if (G > sms) continue;
     for (int L : Ls)
       for (int sl : sleeps) {
-        cudaMemset(recs, 0, (size_t)NB * 160 * NS * 8);
+        cudaMemset(recs, 0, ((size_t)NB * 160 * NS + NB) * 8);
         void* args[] = {&recs, (void*)&E, (void*)&L, (void*)&sl, &tout};
         int Ev = E;
         args[1] = &Ev;
@@ -168,7 +217,7 @@ int main(int argc, char** argv) {
         args[3] = &slv;
         cudaEventRecord(a);
         void* fn = mode == 0 ? (void*)k_sync<0> : mode == 1 ? (void*)k_sync<1>
-                 : mode == 2 ? (void*)k_sync<2> : (void*)k_sync<3>;
+                 : mode == 2 ? (void*)k_sync<2> : mode == 4 ? (void*)k_sync<4> : (void*)k_sync<3>;
         cudaLaunchCooperativeKernel(fn, dim3(G), dim3(64), args, 0, 0);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
