@@ -58,6 +58,27 @@ constexpr int kGRed = 8;      // CTA-reduction slots (events)
 #ifndef SYSCD_GRID_SLEEP
 #define SYSCD_GRID_SLEEP 256  // reducer poll back-off (ns)
 #endif
+// Fixed-point exchange (default): the grid totals are summed by the L2 atomic
+// units.  Every CTA adds (llrint(partial * 2^shift) << 8) + 1 into the event's
+// NS accumulator words with red.add.u64; integer addition is associative, so
+// the total is independent of arrival order (bit-identical in every CTA and
+// run to run), and the low byte counts the contributions: a word whose low
+// byte advanced by G since the slot's previous event is complete.  A reducer
+// polls ONE 32-byte sector per event instead of G records (publish -> totals
+// across 145 CTAs: 1.55-1.8 us against 2.9-3.1 us, scripts/grid_sync.cu, and
+// no poll traffic competing with the A stream).  The shifts are powers of two
+// derived from Cauchy-Schwarz bounds every CTA computes identically:
+//   Gram words   |x_i . x_k| <= max_j q_j                    (fixed per launch)
+//   s words      |x_e . w|  <= sqrt(max_j q_j) ||w||, with ||w||^2 tracked
+//                exactly from the resolved steps (||w + t x||^2 = ||w||^2 +
+//                t (2 x.w + t q)), starting from d max_i |u_i|^2.
+// The sums over CTAs obey the same bounds, so 55 bits never overflow; the
+// resolution is >= 2^-52 of the bound, far below the fp32 rounding of the
+// partials themselves.  SYSCD_GRID_FXP=0 builds the tagged-float records.
+#ifndef SYSCD_GRID_FXP
+#define SYSCD_GRID_FXP 1
+#endif
+constexpr int kGSlotWords = 32;  // fixed-point: 64-bit words per event slot (one 256-byte line pair)
 
 struct GridArgs {
   const float* A;
@@ -91,7 +112,7 @@ __device__ __forceinline__ unsigned long long gtimer_g() {
 }
 
 struct GridSmem {
-  size_t ring, full, empty, totbar, tot, red, meta, recent, total;
+  size_t ring, full, empty, totbar, tot, red, meta, recent, prev, total;
 };
 
 __host__ __device__ inline size_t galign(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -116,6 +137,10 @@ __host__ __device__ inline GridSmem grid_smem(int stages, int cta_rows, int ns) 
   o += kGMeta * 16;
   L.recent = o;
   o += 16 * kGRecent * 8;  // one ring per math warp (<= 16 warps)
+  L.prev = o;
+#if SYSCD_GRID_FXP
+  o += (size_t)kGNB * ns * 8;  // accumulator words at each slot's previous event
+#endif
   L.total = galign(o, 128);
   return L;
 }
@@ -130,6 +155,23 @@ __device__ __forceinline__ unsigned long long ld_tagged(const unsigned long long
   unsigned long long w;
   asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
   return w;
+}
+
+__device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long long w) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// 2^sh as a float (sh clamped to the normal range) and the power-of-two pair
+// (scale, 1/scale) for a bound whose biased float exponent sum is known
+__device__ __forceinline__ float pow2f(int sh) {
+  sh = sh < -100 ? -100 : (sh > 100 ? 100 : sh);
+  return __int_as_float((sh + 127) << 23);
 }
 
 // Sum NV values (NV a power of two <= 32) over a warp with log2(NV) halving
@@ -228,6 +270,9 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
   float* red = reinterpret_cast<float*>(smem + Lo.red);
   int4* meta = reinterpret_cast<int4*>(smem + Lo.meta);
   int2* recent = reinterpret_cast<int2*>(smem + Lo.recent);
+#if SYSCD_GRID_FXP
+  unsigned long long* prevw = reinterpret_cast<unsigned long long*>(smem + Lo.prev);
+#endif
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -265,6 +310,55 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
     fence_proxy_async();
   }
   __syncthreads();
+
+#if SYSCD_GRID_FXP
+  // ---- the launch's fixed-point bounds (identical in every CTA: max is
+  // order-independent).  qmax over the columns of this launch; wmax over u
+  // (every partition starts from w = u), exchanged once through the workspace.
+  float qmax_b, w2_init;
+  {
+    float* scr = red;  // scratch before the event loop uses it
+    float qm = 0.f, wm = 0.f;
+    for (int64_t q = s_begin + tid; q < s_end; q += blockDim.x)
+      qm = fmaxf(qm, fabsf(__ldg(A.sq + A.seq[q])));
+    const int64_t r_end = min(d, row0 + cta_rows);
+    for (int64_t r = row0 + tid; r < r_end; r += blockDim.x) wm = fmaxf(wm, fabsf(__ldg(A.u + r)));
+    qm = warp_max(qm);
+    wm = warp_max(wm);
+    if (lane == 0) {
+      scr[warp] = qm;
+      scr[32 + warp] = wm;
+    }
+    __syncthreads();
+    unsigned int* gw = reinterpret_cast<unsigned int*>(A.recs + (size_t)kGNB * kGSlotWords);
+    if (tid == 0) {
+      for (int q = 1; q < NWT; ++q) {
+        qm = fmaxf(qm, scr[q]);
+        wm = fmaxf(wm, scr[32 + q]);
+      }
+      atomicMax(gw, __float_as_uint(wm));  // non-negative floats order like their bits
+      __threadfence();
+      atomicAdd(gw + 2, 1u);
+      unsigned int seen;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(gw + 2) : "memory");
+      } while (seen < (unsigned)G);
+      scr[0] = qm;
+      scr[32] = __uint_as_float(__ldcg(gw));
+    }
+    __syncthreads();
+    qmax_b = fmaxf(scr[0], 8.6736174e-19f);  // floors (2^-60) keep the shifts in the normal range
+    const float wg = scr[32];
+    w2_init = fmaxf((float)d * wg * wg, 8.6736174e-19f);
+    __syncthreads();  // scr is the CTA-reduction ring from here on
+  }
+  // Gram words: |g| <= qmax < 2^(eq+1)  ->  |g| 2^shG < 2^52
+  const int eq_b = (__float_as_int(qmax_b) >> 23) - 127;
+  const float invG = pow2f(eq_b + 1 - 52);
+  // s words: |s| <= sqrt(qmax W) < 2^((eq + ew + 3) >> 1) with ew the unbiased
+  // exponent of W  ->  shS = 52 - ((eq + ew + 3) >> 1); c0 folds the bias
+  const int c0_b = eq_b + 3 - 127;
+#endif
 
   // ------------------------------------------------------------ reducer state
   // Each reducer warp keeps RSL events in flight (reducer w, slot k takes
@@ -418,11 +512,62 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
       while (s < s_end) produce();
     } else {
       // ------------------------------------------------------------ reducers
+#if SYSCD_GRID_FXP
+      // Lane l watches word l % NP of the event of group l / NP (events r with
+      // r % D == group; D events per load instruction), and the events are
+      // handed over in order.  A word is complete when its low byte advanced
+      // by G since the slot's previous event; the event total is the
+      // difference of the two 64-bit values (exact modulo 2^64) without that
+      // byte.
+      constexpr int D = 32 / NP;
+      const int c = lane % NP, k = lane / NP;
+      const bool act = c < NS;
+      for (int i = lane; i < kGNB * NS; i += 32) prevw[i] = 0ull;
+      __syncwarp();
+      int64_t r_me = k, r0 = 0;
+      unsigned long long cur = 0ull;
+      bool have = false;
+      const unsigned long long gcount = (unsigned long long)(G & 0xFF);
+      if (rw > 0) r0 = events;  // one warp gathers every event (a sector per event)
+      while (r0 < events) {
+        if (act && !have && r_me < events && r_me <= r0 + LL + 1) {
+          cur = ld_tagged(A.recs + (size_t)(r_me % kGNB) * kGSlotWords + c);
+          have = ((cur - prevw[(r_me % kGNB) * NS + c]) & 0xFFull) == gcount;
+        }
+        unsigned m = __ballot_sync(0xffffffffu, have || !act);
+        bool prog = false;
+        while (r0 < events) {
+          const int g = (int)(r0 % D);
+          const unsigned gm = (NP == 32 ? 0xffffffffu : ((1u << NP) - 1u)) << (g * NP);
+          if ((m & gm) != gm) break;
+          if (k == g && act) {
+            unsigned long long* pw = prevw + (r0 % kGNB) * NS + c;
+            const long long total = (long long)(cur - *pw) >> 8;
+            *pw = cur;
+            tot[(r0 % kGTot) * kGVal + c] = __ll2float_rn(total);
+            have = false;
+            r_me += D;
+          }
+          m &= ~gm;  // the group's next event has not been polled yet
+          __syncwarp();
+          if (lane == 0) {
+#ifdef SYSCD_TRACE
+            if (A.dbg && r0 < 1024) A.dbg[8192 + 1024 * 160 + r0 * 160 + cta] = gtimer_g();
+#endif
+            mbar_arrive(&totbar[r0 % kGTot]);
+          }
+          ++r0;
+          prog = true;
+        }
+        if (!prog) __nanosleep(SYSCD_GRID_SLEEP);
+      }
+#else
       for (;;) {
         bool prog = false;
         if (!reduce_pass(rs_ev, wv, events, &prog)) break;
         if (!prog) __nanosleep(SYSCD_GRID_SLEEP);
       }
+#endif
     }
   } else {
     // -------------------------------------------------------------- math warps
@@ -442,6 +587,16 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
         for (int r = 0; r < RR; ++r) xr[sl][b][r] = 0.f;
     const float a = A.a;
     const float inv_a = (float)(1.0 / A.a_d);
+#if SYSCD_GRID_FXP
+    float w2 = w2_init, w2max = w2_init;  // ||w||^2 (tracked) and its running maximum
+    float invS[NSLOT];                     // 2^-shS of the event in each register slot
+#pragma unroll
+    for (int sl = 0; sl < NSLOT; ++sl) invS[sl] = 1.f;
+    const float aG = a * invG;  // Gram totals are decoded inside the step's a * delta factor
+    const float scaleG = __int_as_float(0x7F000000 - __float_as_int(invG));
+#else
+    const float aG = a;
+#endif
     uint32_t stage = 0, phase = 0;
     bool flushed = false;
     int64_t ebase = 0;  // event (publication) index of the partition's block 0
@@ -590,11 +745,28 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
               if (A.dbg && warp == 0 && lane == 0 && pub < 1024)
                 A.dbg[8192 + pub * 160 + cta] = gtimer_g();
 #endif
+#if SYSCD_GRID_FXP
+              // this event's s-scale from the running bound on ||w||^2 (the w of
+              // the partials above: every step resolved so far is tracked)
+              invS[i] = __int_as_float((127 - 52 + ((c0_b + (__float_as_int(w2max) >> 23)) >> 1)) << 23);
+#endif
               if (warp == 0 && lane < NS) {
                 float v = 0.f;
                 for (int q = 0; q < NWC; ++q) v += rslot[q * NS + lane];
+#if SYSCD_GRID_FXP
+                const float sc =
+                    lane < BB ? __int_as_float(0x7F000000 - __float_as_int(invS[i])) : scaleG;
+                float f = v * sc;
+                if (!(fabsf(f) < 1.8014399e16f)) {  // 2^54: NaN/Inf or bounds violated (bad sq)
+                  atomicOr(A.status, SYSCD_ENONFINITE);
+                  f = 0.f;
+                }
+                red_add_u64(A.recs + (size_t)(pub % kGNB) * kGSlotWords + lane,
+                            ((unsigned long long)__float2ll_rn(f) << 8) + 1ull);
+#else
                 st_tagged(A.recs + (size_t)(pub % kGNB) * kGVal * G + GREC_IDX(lane, cta),
                           (uint32_t)(pub + 1), v);
+#endif
 #ifdef SYSCD_GRID_DCHK
                 if (A.dbg && pub < 8192)  // every CTA's published partials
                   A.dbg[8192 + 2 * 1024 * 160 + 1024 * 160 * 8 + 8192 * 160 +
@@ -616,14 +788,18 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
                 dcur[b] = 0.f;
                 const int col = c * BB + b;
                 if (col < m) {
+#if SYSCD_GRID_FXP
+                  float lin = t[Lay::kS + b] * invS[XS_RES];
+#else
                   float lin = t[Lay::kS + b];
+#endif
 #pragma unroll
                   for (int l = 1; l <= LL; ++l)
 #pragma unroll
                     for (int k = 0; k < BB; ++k)
-                      lin = fmaf(a * dh[l - 1][k], t[Lay::gx(l, b, k)], lin);
+                      lin = fmaf(aG * dh[l - 1][k], t[Lay::gx(l, b, k)], lin);
 #pragma unroll
-                  for (int k = 0; k < b; ++k) lin = fmaf(a * dcur[k], t[Lay::gin(b, k)], lin);
+                  for (int k = 0; k < b; ++k) lin = fmaf(aG * dcur[k], t[Lay::gin(b, k)], lin);
                   const int4 mt = meta[(col0 + col) & (kGMeta - 1)];
                   const int j = mt.x;
                   float aj = __int_as_float(mt.y);
@@ -648,6 +824,13 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
                   }
                   if (isfinite(an)) {
                     dcur[b] = an - aj;
+#if SYSCD_GRID_FXP
+                    {  // ||w + t x||^2 = ||w||^2 + t (2 x.w + t q), t = a delta
+                      const float tq = a * dcur[b];
+                      w2 = fmaf(tq, fmaf(tq, qj, lin + lin), w2);
+                      w2max = fmaxf(w2max, w2);
+                    }
+#endif
                     if (cta == 0 && tid == 0) __stcg(A.alpha + j, an);
                   } else if (cta == 0 && tid == 0) {
                     atomicOr(A.status, SYSCD_ENONFINITE);
@@ -711,6 +894,9 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
           w[r] = uu;
         }
       }
+#if SYSCD_GRID_FXP
+      w2 = w2_init;
+#endif
       flushed = true;
     }
     if (!flushed) {
@@ -812,7 +998,7 @@ int grid_choose(int64_t d, int* idx, int* G, int* stages, size_t* smem_out, int6
   return SYSCD_EINVAL;
 }
 
-int64_t grid_workspace_bytes(int G) { return (int64_t)kGNB * kGVal * G * 8; }
+int64_t grid_workspace_bytes(int G) { return (int64_t)kGNB * kGVal * (G + 1) * 8; }
 
 int grid_launch(const syscd_dense_epoch_args* e, void* workspace, int64_t ws_bytes,
                 cudaStream_t stream) {
@@ -857,7 +1043,11 @@ int grid_launch(const syscd_dense_epoch_args* e, void* workspace, int64_t ws_byt
   A.recs = (unsigned long long*)workspace;
   A.status = e->status;
   A.dbg = (unsigned long long*)g_grid_dbg;
+#if SYSCD_GRID_FXP
+  SYSCD_CUDA_TRY(cudaMemsetAsync(A.recs, 0, ((size_t)kGNB * kGSlotWords + 8) * 8, stream));
+#else
   SYSCD_CUDA_TRY(cudaMemsetAsync(A.recs, 0, grid_workspace_bytes(G), stream));
+#endif
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(G, 1, 1);
   cfg.blockDim = dim3(ge.nthreads, 1, 1);

@@ -8,7 +8,11 @@
 // the per-event time is the exchange chain / (L + 1).  Pollers: MODE 0 one
 // event at a time; 1 k_grid_epoch's two-slot sequential poller; 2 two events
 // in flight, both issued per pass; 4 leader protocol (CTA 0 gathers and
-// broadcasts one word per event).
+// broadcasts one word per event); 5 fixed-point atomic exchange: every CTA adds
+// (value << 8) + 1 into the event's NS accumulator words with red.add.u64 (the
+// L2 sums; integer, so order-independent), the poller reads one 32-byte sector
+// and an event is complete when the low byte advanced by G (up to 8 events per
+// poll instruction); 6 the same with each word on its own 256-byte line.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/grid_sync scripts/grid_sync.cu
 //   /tmp/grid_sync
 #include <cstdio>
@@ -27,6 +31,10 @@ __device__ __forceinline__ unsigned long long ld_rel(const unsigned long long* p
   unsigned long long w;
   asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
   return w;
+}
+
+__device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long long w) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
 }
 
 template <int MODE>
@@ -48,9 +56,48 @@ __global__ void k_sync(unsigned long long* recs, int E, int L, int sleep_ns, uns
         }
       __syncwarp();
       if (lane < NS) {
-        const unsigned long long w = ((unsigned long long)(e + 1) << 32) | (unsigned)(cta + lane);
-        st_rel(recs + ((size_t)(e % NB) * G + cta) * NS + lane, w);
+        if (MODE >= 5) {
+          const size_t stride = MODE == 6 ? 32 : 1;  // words between an event's values
+          const unsigned long long fx = (unsigned long long)(long long)(cta - 70 + lane + e);
+          red_add_u64(recs + ((size_t)(e % NB) * NS + lane) * stride * (MODE == 6 ? 1 : 1) +
+                          (MODE == 5 ? (size_t)(e % NB) * 28 : 0),
+                      (fx << 8) + 1ull);
+        } else {
+          const unsigned long long w = ((unsigned long long)(e + 1) << 32) | (unsigned)(cta + lane);
+          st_rel(recs + ((size_t)(e % NB) * G + cta) * NS + lane, w);
+        }
       }
+    }
+  } else if (MODE >= 5) {
+    // accumulator poller: lane l watches word l % NS of event r0 + l / NS
+    // (32 / NS events per load instruction), hands over in order.  prev = the
+    // word's value when its previous event (r - NB) completed.
+    __shared__ unsigned long long prev[NB][NS];
+    if (lane < NS)
+      for (int s = 0; s < NB; ++s) prev[s][lane] = 0ull;
+    __syncwarp();
+    const size_t stride = MODE == 6 ? 32 : 1;
+    const int c = lane % NS, k = lane / NS;
+    constexpr int D = 4;  // events in flight per pass
+    int r0 = 0;
+    while (r0 < E) {
+      const int r = r0 + k;
+      bool ok = true;
+      unsigned long long cur = 0;
+      if (k < D && r < E) {
+        cur = ld_rel(recs + ((size_t)(r % NB) * NS + c) * stride + (MODE == 5 ? (size_t)(r % NB) * 28 : 0));
+        ok = ((cur - prev[r % NB][c]) & 0xFFull) == (unsigned long long)(G & 0xFF);
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, ok);
+      // events complete in order from r0
+      int nd = 0;
+      while (nd < D && r0 + nd < E && ((m >> (nd * NS)) & ((1u << NS) - 1)) == ((1u << NS) - 1)) ++nd;
+      if (k < nd) prev[r % NB][c] = cur;
+      __syncwarp();
+      if (lane == 0)
+        for (int q = 0; q < nd; ++q) fin[(r0 + q) % NB] = r0 + q + 1;
+      r0 += nd;
+      if (nd == 0 && sleep_ns > 0) __nanosleep(sleep_ns);
     }
   } else if (MODE == 4) {
     // leader protocol: CTA 0 gathers every record of event r and publishes one
@@ -199,11 +246,11 @@ int main(int argc, char** argv) {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  const int Gs[] = {145};
+  const int Gs[] = {145, 148};
   const int Ls[] = {1, 2, 3};
-  const int sleeps[] = {0, 256};
+  const int sleeps[] = {0, 64, 256};
   printf("mode(events in flight) G L sleep_ns us_per_event\n");
-  for (int mode : {1, 2, 4})
+  for (int mode : {1, 2, 5, 6})
   for (int G : Gs) {
     if (G > sms) continue;
     for (int L : Ls)
@@ -217,7 +264,8 @@ int main(int argc, char** argv) {
         args[3] = &slv;
         cudaEventRecord(a);
         void* fn = mode == 0 ? (void*)k_sync<0> : mode == 1 ? (void*)k_sync<1>
-                 : mode == 2 ? (void*)k_sync<2> : mode == 4 ? (void*)k_sync<4> : (void*)k_sync<3>;
+                 : mode == 2 ? (void*)k_sync<2> : mode == 4 ? (void*)k_sync<4>
+                 : mode == 5 ? (void*)k_sync<5> : mode == 6 ? (void*)k_sync<6> : (void*)k_sync<3>;
         cudaLaunchCooperativeKernel(fn, dim3(G), dim3(64), args, 0, 0);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
