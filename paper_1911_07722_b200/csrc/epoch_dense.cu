@@ -562,7 +562,8 @@ struct Choice {
   int grid;  // 1: grid-wide lookahead kernel (epoch_grid.cu)
 };
 
-int grid_choose(int64_t d, int* idx, int* G, int* stages, size_t* smem_out, int64_t* cta_rows);
+int grid_choose(int64_t d, int* idx, int* G, int* stages, size_t* smem_out, int64_t* cta_rows,
+                int iid);
 int small_workers(int32_t n_parts);
 int small_launch(const syscd_dense_epoch_args* e, cudaStream_t stream);
 bool mid_applicable(int64_t d, int32_t n_parts, int* workers, int* cluster);
@@ -612,7 +613,7 @@ static int choose(int64_t d, int32_t n_parts, Choice* out) {
   // clusters (one partition then streams over every SM instead of one GPC).
   int gidx, gG, gst;
   size_t gsm;
-  const bool grid_ok = grid_choose(d, &gidx, &gG, &gst, &gsm, nullptr) == SYSCD_OK;
+  const bool grid_ok = grid_choose(d, &gidx, &gG, &gst, &gsm, nullptr, 1) == SYSCD_OK;
   if (grid_ok && (bc.idx < 0 || (d >= 131072 && bc.G < 4 && n_parts < 4))) {
     *out = {gidx, 1, 1, gst, gsm, 1};
     return SYSCD_OK;
@@ -670,7 +671,7 @@ extern "C" int64_t syscd_dense_epoch_workspace_bytes(int64_t d, int32_t n_parts)
   if (!ch.grid) return 0;
   int idx, G, st;
   size_t sm;
-  grid_choose(d, &idx, &G, &st, &sm, nullptr);
+  grid_choose(d, &idx, &G, &st, &sm, nullptr, 1);
   return grid_workspace_bytes(G);
 }
 

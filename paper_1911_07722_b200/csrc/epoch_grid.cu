@@ -78,6 +78,9 @@ constexpr int kGRed = 8;      // CTA-reduction slots (events)
 #ifndef SYSCD_GRID_FXP
 #define SYSCD_GRID_FXP 1
 #endif
+#ifndef SYSCD_GRID_LATE_RELEASE
+#define SYSCD_GRID_LATE_RELEASE 1  // release a ring stage after the partials consumed it (no proxy fence)
+#endif
 constexpr int kGSlotWords = 32;  // fixed-point: 64-bit words per event slot (one 256-byte line pair)
 
 struct GridArgs {
@@ -117,7 +120,7 @@ struct GridSmem {
 
 __host__ __device__ inline size_t galign(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-__host__ __device__ inline GridSmem grid_smem(int stages, int cta_rows, int ns) {
+__host__ __device__ inline GridSmem grid_smem(int stages, int cta_rows, int ns, int iid) {
   GridSmem L;
   L.ring = 0;
   size_t o = galign((size_t)stages * cta_rows * 4, 128);
@@ -127,6 +130,7 @@ __host__ __device__ inline GridSmem grid_smem(int stages, int cta_rows, int ns) 
   o += (size_t)stages * 8;
   L.totbar = o;
   o += kGTot * 8;
+
   o = galign(o, 16);
   L.tot = o;
   o += kGTot * kGVal * 4;
@@ -136,7 +140,7 @@ __host__ __device__ inline GridSmem grid_smem(int stages, int cta_rows, int ns) 
   L.meta = o;
   o += kGMeta * 16;
   L.recent = o;
-  o += 16 * kGRecent * 8;  // one ring per math warp (<= 16 warps)
+  if (iid) o += 16 * kGRecent * 8;  // iid only: one ring per math warp (<= 16 warps)
   L.prev = o;
 #if SYSCD_GRID_FXP
   o += (size_t)kGNB * ns * 8;  // accumulator words at each slot's previous event
@@ -159,6 +163,26 @@ __device__ __forceinline__ unsigned long long ld_tagged(const unsigned long long
 
 __device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long long w) {
   asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+}
+
+// Two fp32 FMAs in one instruction (FFMA2 on sm_100): same IEEE results per
+// lane as two FFMAs, half the issue slots.
+#ifndef SYSCD_GRID_F2
+#define SYSCD_GRID_F2 2  // 0 never, 1 always, 2 where it measured faster (the LL = 2 wide-warp instance)
+#endif
+__device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
+  unsigned long long p;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(p) : "f"(lo), "f"(hi));
+  return p;
+}
+__device__ __forceinline__ void unpack2(unsigned long long p, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(p));
+}
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
 }
 
 __device__ __forceinline__ float warp_max(float v) {
@@ -247,6 +271,10 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
   static_assert(NRED >= 1, "no reducer warp");
   constexpr int NWC = NTC / 32;
   constexpr int NSLOT = LL + 1;
+  constexpr int PUBW = 0;  // the publishing math warp
+  // packed FMAs (config 3: 5.43 -> 5.38 ms with LL = 2; with LL = 3 they cost registers: 5.48 -> 5.60)
+  constexpr bool F2 = SYSCD_GRID_F2 == 1 || (SYSCD_GRID_F2 == 2 && NWM == 6 && LL == 2 && BB == 1);
+  static_assert(!F2 || (RR % 2 == 0 && SYSCD_GRID_CHAINS == 1), "packed FMAs: even RR, one chain");
   using Lay = GridLayout<BB, LL>;
   constexpr int NS = Lay::kNS;
   static_assert(NS <= kGVal, "event record too large");
@@ -261,7 +289,7 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
 
   extern __shared__ __align__(128) unsigned char smem[];
   const int S = A.stages;
-  const GridSmem Lo = grid_smem(S, CTA_ROWS, NS);
+  const GridSmem Lo = grid_smem(S, CTA_ROWS, NS, IID ? 1 : 0);
   float* ring = reinterpret_cast<float*>(smem + Lo.ring);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Lo.full);
   uint64_t* empty = reinterpret_cast<uint64_t*>(smem + Lo.empty);
@@ -292,7 +320,8 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
   // proxy) fills that follow the barrier; one fence by the issuing thread
   // does not cover the other threads' writes
   fence_proxy_async();
-  for (int i = tid; i < 16 * kGRecent; i += blockDim.x) recent[i] = make_int2(-1, 0);
+  if (IID)
+    for (int i = tid; i < 16 * kGRecent; i += blockDim.x) recent[i] = make_int2(-1, 0);
 #if defined(SYSCD_TRACE) && defined(SYSCD_TRACE_LIGHT)
   if (A.dbg && tid == 0) {  // SM of every CTA (scripts/grid_skew.py)
     unsigned smid;
@@ -598,6 +627,10 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
     const float aG = a;
 #endif
     uint32_t stage = 0, phase = 0;
+#ifdef SYSCD_GRID_CLK
+    long long clk_acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    long long clk_last = clock64();
+#endif
     bool flushed = false;
     int64_t ebase = 0;  // event (publication) index of the partition's block 0
     // iid: the prefetched alpha of a coordinate drawn again within the
@@ -616,7 +649,7 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
 #pragma unroll
         for (int b = 0; b < BB; ++b) dh[l][b] = 0.f;
 #define XS_OLD(l) ((i + NSLOT - (l)) % NSLOT)
-#define XS_RES ((i + 1) % NSLOT)
+#define XS_RES ((i + NSLOT - LL) % NSLOT)
       for (int e0 = 0; e0 < nb + LL; e0 += NSLOT) {
 #pragma unroll
         for (int i = 0; i < NSLOT; ++i) {
@@ -640,34 +673,67 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
   do {            \
   } while (0)
 #endif
+#ifdef SYSCD_GRID_CLK  // experiment: per-phase SM cycles of a few warps (printf at the end)
+#define GCLK(k)                         \
+  do {                                  \
+    const long long t_ = clock64();     \
+    clk_acc[k] += t_ - clk_last;        \
+    clk_last = t_;                      \
+  } while (0)
+#else
+#define GCLK(k) \
+  do {          \
+  } while (0)
+#endif
             GSTAMP(0);
+            GCLK(0);
+            // One iteration: stage block e and publish its partials, then resolve
+            // block e - LL from its grid totals.  (Resolving first, so that the
+            // warp reduction and the axpy share a basic block, was measured:
+            // 5.80 against 5.47 ms on config 3 -- the publication then waits for
+            // one more set of totals.)
             if (e < nb) {
               // ---- stage block e and publish its partials
+              // A ring stage is copied to registers and released LATE: after
+              // the warp reduction below, through an arrive that takes the
+              // reduced value as an operand.  Every loaded register has then
+              // been consumed by an FMA the warp issued, so the loads have
+              // landed and the TMA refill (async proxy) cannot overtake them
+              // -- an arrive right after the loads can (config 3 went
+              // nondeterministic once the grid ran fast enough), and the
+              // proxy fence that prevents it serialises loads and FMAs
+              // (SYSCD_GRID_LATE_RELEASE=0: 5.72 against 5.47 ms on config 3).
+              auto load_col = [&](float (&dst)[RR]) -> uint64_t* {
+                mbar_wait(&full[stage], phase);
+                const float* x = ring + (size_t)stage * CTA_ROWS + tid;
+#pragma unroll
+                for (int r = 0; r < RR; ++r) dst[r] = x[r * NTC];
+                uint64_t* bar = &empty[stage];
+#if !SYSCD_GRID_LATE_RELEASE
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bar);
+#endif
+                if (++stage == (uint32_t)S) {
+                  stage = 0;
+                  phase ^= 1u;
+                }
+                return bar;
+              };
+              GCLK(7);
+              uint64_t* rel[BB];
 #pragma unroll
               for (int b = 0; b < BB; ++b) {
                 if (e * BB + b < m) {
-                  mbar_wait(&full[stage], phase);
-                  const float* x = ring + (size_t)stage * CTA_ROWS + tid;
-#pragma unroll
-                  for (int r = 0; r < RR; ++r) xr[i][b][r] = x[r * NTC];
-                  // the TMA refill of this stage (async proxy) must not overtake
-                  // these generic-proxy reads: without the proxy fence the arrive
-                  // can complete while the loads are still in flight, and a warp
-                  // then reads part of the next column (config 3 went
-                  // nondeterministic once the grid ran fast enough)
-                  fence_proxy_async();
-                  __syncwarp();
-                  if (lane == 0) mbar_arrive(&empty[stage]);
-                  if (++stage == (uint32_t)S) {
-                    stage = 0;
-                    phase ^= 1u;
-                  }
+                  rel[b] = load_col(xr[i][b]);
                 } else {
+                  rel[b] = nullptr;
 #pragma unroll
                   for (int r = 0; r < RR; ++r) xr[i][b][r] = 0.f;
                 }
               }
               GSTAMP(1);
+              GCLK(1);
 #ifdef SYSCD_GRID_DCHK
               if (A.dbg && ebase + e < 8192) {  // integer checksums of x_e and w per CTA
                 unsigned int cx = 0, cw = 0;
@@ -701,6 +767,36 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
 #ifdef SYSCD_GRID_NOMATH  // experiment: data-delivery ceiling (wrong results)
               prc[0][0] = xr[i][0][0];
 #else
+              if constexpr (F2) {  // rows in pairs through FFMA2 (even / odd rows accumulate apart)
+                unsigned long long p2[NS];
+#pragma unroll
+                for (int k = 0; k < NS; ++k) p2[k] = 0ull;
+#pragma unroll
+                for (int r = 0; r < RR; r += 2) {
+#pragma unroll
+                  for (int b = 0; b < BB; ++b) {
+                    const unsigned long long xv = pack2(xr[i][b][r], xr[i][b][r + 1]);
+                    p2[Lay::kS + b] = ffma2(xv, pack2(w[r], w[r + 1]), p2[Lay::kS + b]);
+#pragma unroll
+                    for (int k = 0; k < b; ++k)
+                      p2[Lay::gin(b, k)] =
+                          ffma2(xv, pack2(xr[i][k][r], xr[i][k][r + 1]), p2[Lay::gin(b, k)]);
+#pragma unroll
+                    for (int l = 1; l <= LL; ++l)
+#pragma unroll
+                      for (int k = 0; k < BB; ++k)
+                        p2[Lay::gx(l, b, k)] =
+                            ffma2(xv, pack2(xr[XS_OLD(l)][k][r], xr[XS_OLD(l)][k][r + 1]),
+                                  p2[Lay::gx(l, b, k)]);
+                  }
+                }
+#pragma unroll
+                for (int k = 0; k < NS; ++k) {
+                  float lo, hi;
+                  unpack2(p2[k], lo, hi);
+                  prc[0][k] = lo + hi;
+                }
+              } else {
 #pragma unroll
               for (int r = 0; r < RR; ++r) {
                 float* pr = prc[r % NCH];
@@ -719,6 +815,7 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
                           fmaf(xv, xr[XS_OLD(l)][k][r], pr[Lay::gx(l, b, k)]);
                 }
               }
+              }
 #endif
               float pr[NS];
 #pragma unroll
@@ -727,8 +824,9 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
 #pragma unroll
                 for (int h = 1; h < NCH; ++h) pr[k] += prc[h][k];
               }
+              GCLK(2);
               // warp totals (shuffle-transposed: NP-1 + 5-log2(NP) shuffles
-              // instead of 5*NS), then warp 0 sums the warps' deposits in
+              // instead of 5*NS), then one warp sums the warps' deposits in
               // warp order and publishes the CTA's record
               const int64_t pub = ebase + e;
               float* rslot = red + (size_t)(pub % kGRed) * 16 * NS;
@@ -736,13 +834,23 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
 #pragma unroll
               for (int k = 0; k < NP; ++k) pv[k] = k < NS ? pr[k] : 0.f;
               const float tv = warp_sum_multi<NP>(pv, lane);
+              GCLK(3);
+#if SYSCD_GRID_LATE_RELEASE
+              if (lane == 0) {
+#pragma unroll
+                for (int b = 0; b < BB; ++b)
+                  if (rel[b])
+                    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];  // after %1"
+                                 ::"r"(smem_addr(rel[b])), "f"(tv) : "memory");
+              }
+#endif
               {
                 const int idx = multi_index<NP>(lane);
                 if ((lane & (32 / NP - 1)) == 0 && idx < NS) rslot[warp * NS + idx] = tv;
               }
               named_bar_sync(1, NTC);
 #ifdef SYSCD_TRACE
-              if (A.dbg && warp == 0 && lane == 0 && pub < 1024)
+              if (A.dbg && warp == PUBW && lane == 0 && pub < 1024)
                 A.dbg[8192 + pub * 160 + cta] = gtimer_g();
 #endif
 #if SYSCD_GRID_FXP
@@ -750,7 +858,7 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
               // the partials above: every step resolved so far is tracked)
               invS[i] = __int_as_float((127 - 52 + ((c0_b + (__float_as_int(w2max) >> 23)) >> 1)) << 23);
 #endif
-              if (warp == 0 && lane < NS) {
+              if (warp == PUBW && lane < NS) {
                 float v = 0.f;
                 for (int q = 0; q < NWC; ++q) v += rslot[q * NS + lane];
 #if SYSCD_GRID_FXP
@@ -775,12 +883,14 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
               }
             }
             GSTAMP(2);
+            GCLK(5);
             if (e >= LL) {
-              // ---- resolve block c = e - LL (register slot (i + 1) % NSLOT)
+              // ---- resolve block c = e - LL (register slot XS_RES)
               const int c = e - LL;
               const int64_t cpub = ebase + c;
               mbar_wait(&totbar[cpub % kGTot], (uint32_t)((cpub / kGTot) & 1));
               GSTAMP(3);
+              GCLK(6);
               const float* t = tot + (cpub % kGTot) * kGVal;
               float dcur[BB];
 #pragma unroll
@@ -855,11 +965,22 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
 #pragma unroll
               for (int b = 0; b < BB; ++b) {
                 const float sd = a * dcur[b];
+                if constexpr (F2) {
+                  const unsigned long long sd2 = pack2(sd, sd);
 #pragma unroll
-                for (int r = 0; r < RR; ++r) w[r] = fmaf(sd, xr[XS_RES][b][r], w[r]);
+                  for (int r = 0; r < RR; r += 2) {
+                    const unsigned long long wn = ffma2(
+                        sd2, pack2(xr[XS_RES][b][r], xr[XS_RES][b][r + 1]), pack2(w[r], w[r + 1]));
+                    unpack2(wn, w[r], w[r + 1]);
+                  }
+                } else {
+#pragma unroll
+                  for (int r = 0; r < RR; ++r) w[r] = fmaf(sd, xr[XS_RES][b][r], w[r]);
+                }
               }
             }
             GSTAMP(4);
+            GCLK(8);
 #if (defined(SYSCD_TRACE) && !defined(SYSCD_TRACE_LIGHT)) || defined(SYSCD_GRID_DCHK)
             if (A.dbg && tid == 0 && e >= LL && ebase + e - LL < 8192) {
               // every event's first delta per CTA (divergence check)
@@ -904,6 +1025,14 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
       for (int r = 0; r < RR; ++r)
         if (r < rmax) outp[r * NTC] = 0.f;
     }
+#ifdef SYSCD_GRID_CLK
+    if (lane == 0 && (cta == 0 || cta == 77) && ebase > 0)
+      printf("clk cta %d warp %d events %lld: loop %lld | wait-full+lds %lld | fma %lld | warpsum %lld | "
+             "release+deposit+bar+publish %lld | wait-tot %lld | resolve+axpy %lld (cycles/event)\n",
+             cta, warp, (long long)ebase, clk_acc[0] / ebase, (clk_acc[7] + clk_acc[1]) / ebase,
+             clk_acc[2] / ebase, clk_acc[3] / ebase, clk_acc[5] / ebase, clk_acc[6] / ebase,
+             clk_acc[8] / ebase);
+#endif
   }
 }
 
@@ -949,13 +1078,19 @@ static GridEntry g_grid_table[] = {
     // <24,1,3,9 of 12 warps> 5.89, <22,1,3,10/12> 7.46, <27,1,2,8/12> 10.8,
     // <36,1,4,6/8> 7.44 ms (255 registers); fewer, longer slices
     // <38,1,3,6/8> (138 CTAs) 5.92, <40,...> (131) 5.99, <43,1,3,5/7> 6.39.
+    // With the fixed-point exchange the totals arrive early enough for
+    // LL = 2 (one FMA per row less, room for packed FMAs): 5.38 against 5.48
+    // ms.  LL = 3 stays reachable (SYSCD_GRID_CFG=5): it is bound by the
+    // CTA's own work per event, LL = 2 by the exchange chain.
+    make_grid<36, 1, 2, 6, 8>(),
     make_grid<36, 1, 3, 6, 8>(),
 };
 constexpr int kGridTable = sizeof(g_grid_table) / sizeof(g_grid_table[0]);
 
 static void* g_grid_dbg = nullptr;
 
-int grid_choose(int64_t d, int* idx, int* G, int* stages, size_t* smem_out, int64_t* cta_rows) {
+int grid_choose(int64_t d, int* idx, int* G, int* stages, size_t* smem_out, int64_t* cta_rows,
+                int iid) {
   int dev = 0, sms = 0, optin = 0;
   SYSCD_CUDA_TRY(cudaGetDevice(&dev));
   SYSCD_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -970,8 +1105,10 @@ int grid_choose(int64_t d, int* idx, int* G, int* stages, size_t* smem_out, int6
     const int rows = g_grid_table[i].ntc * g_grid_table[i].rr;
     const int64_t g = (d + rows - 1) / rows;
     if (g > sms || g > 32 * kNQ) continue;
-    const size_t fixed = grid_smem(0, rows, g_grid_table[i].ns).total + 1024;
-    int s = (int)(((size_t)optin - 1024 - fixed) / ((size_t)rows * 4));
+    // feasibility with the iid layout (the larger one), so the geometry does
+    // not depend on the sampling mode
+    const size_t fixed = grid_smem(0, rows, g_grid_table[i].ns, 1).total;
+    int s = (int)(((size_t)optin - fixed) / ((size_t)rows * 4));
     s = std::min(s, 8);
     if (s < g_grid_table[i].bb + 2) continue;
     if (g > best_g) {
@@ -984,12 +1121,24 @@ int grid_choose(int64_t d, int* idx, int* G, int* stages, size_t* smem_out, int6
     const int rows = g_grid_table[best].ntc * g_grid_table[best].rr;
     *idx = best;
     *G = best_g;
+    // the kernel has no static shared memory: everything up to the opt-in
+    // limit goes to the ring (the iid layout carries the recently-resolved
+    // rings; without them config 3 gets an 8th stage)
+    {
+      const size_t fixed = grid_smem(0, rows, g_grid_table[best].ns, iid).total;
+      best_s = std::min((int)(((size_t)optin - fixed) / ((size_t)rows * 4)), 8);
+      if (const char* fs = getenv("SYSCD_GRID_STAGES")) best_s = std::min(best_s, atoi(fs));
+    }
     *stages = best_s;
-    *smem_out = grid_smem(best_s, rows, g_grid_table[best].ns).total;
+    *smem_out = grid_smem(best_s, rows, g_grid_table[best].ns, iid).total;
     // Slices are the entry's full capacity.  Spreading d over every SM
     // (148 slices of 6784 rows instead of 145 of 6912, 128-byte aligned or
     // not) measured slower on config 3: 6.01 against 5.80 ms per epoch.
-    const int64_t cr = rows;
+    int64_t cr = rows;
+    if (const char* fr = getenv("SYSCD_GRID_ROWS")) {  // experiments: shorter slices on more SMs
+      const int64_t r = atoll(fr) / 4 * 4;
+      if (r >= 4 && r <= rows && (d + r - 1) / r <= sms) cr = r;
+    }
     if (cta_rows) *cta_rows = cr;
     *G = (int)((d + cr - 1) / cr);
     return SYSCD_OK;
@@ -1005,7 +1154,7 @@ int grid_launch(const syscd_dense_epoch_args* e, void* workspace, int64_t ws_byt
   int idx, G, stages;
   size_t smem;
   int64_t cta_rows = 0;
-  int st = grid_choose(e->d, &idx, &G, &stages, &smem, &cta_rows);
+  int st = grid_choose(e->d, &idx, &G, &stages, &smem, &cta_rows, e->iid ? 1 : 0);
   if (st) return st;
   if (ws_bytes < grid_workspace_bytes(G) || !workspace) {
     set_error("syscd_dense_epoch: grid workspace too small");
