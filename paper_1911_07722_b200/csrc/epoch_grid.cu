@@ -55,9 +55,6 @@ constexpr int kGRed = 8;      // CTA-reduction slots (events)
 #ifndef SYSCD_GRID_TSUM
 #define SYSCD_GRID_TSUM 1  // reducer: all totals in one shuffle-transposed warp sum
 #endif
-#ifndef SYSCD_GRID_SLEEP
-#define SYSCD_GRID_SLEEP 256  // reducer poll back-off (ns)
-#endif
 // Fixed-point exchange (default): the grid totals are summed by the L2 atomic
 // units.  Every CTA adds (llrint(partial * 2^shift) << 8) + 1 into the event's
 // NS accumulator words with red.add.u64; integer addition is associative, so
@@ -77,6 +74,13 @@ constexpr int kGRed = 8;      // CTA-reduction slots (events)
 // partials themselves.  SYSCD_GRID_FXP=0 builds the tagged-float records.
 #ifndef SYSCD_GRID_FXP
 #define SYSCD_GRID_FXP 1
+#endif
+// reducer poll back-off (ns).  The fixed-point reducer polls one sector, so a
+// short back-off costs no L2 bandwidth and the totals are seen sooner (config
+// 3, LL = 2: 0 / 32 / 100 / 256 ns -> 5.27 / 5.28 / 5.28 / 5.38 ms); the
+// tagged-record reducer (G records per poll) keeps 256.
+#ifndef SYSCD_GRID_SLEEP
+#define SYSCD_GRID_SLEEP (SYSCD_GRID_FXP ? 32 : 256)
 #endif
 #ifndef SYSCD_GRID_LATE_RELEASE
 #define SYSCD_GRID_LATE_RELEASE 1  // release a ring stage after the partials consumed it (no proxy fence)
@@ -262,15 +266,22 @@ struct GridLayout {
 // IID: with-replacement sampling (the recently-resolved ring).  Fixing both
 // at compile time takes their branches out of the event loop, whose
 // instruction count bounds this kernel (config 3: 6.51 -> 6.31 ms).
-template <int RR, int BB, int LL, int KIND, bool IID, int NWM, int NWT>
+// EARLY (BB = 1): one more register slot; column e+1 is copied to registers and
+// its Gram cross terms are accumulated right after event e is published, i.e.
+// while the CTA would otherwise wait for grid totals.  Only the s-term FMAs of a
+// block (the ones that need the updated w) then sit between the arrival of the
+// totals and the next publication, which is the chain that bounds the grid.
+template <int RR, int BB, int LL, int KIND, bool IID, int NWM, int NWT, bool EARLY = false>
 __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
+  static_assert(!EARLY || (BB == 1 && RR % 2 == 0 && SYSCD_GRID_FXP && SYSCD_GRID_LATE_RELEASE),
+                "early staging: one column per event, fixed-point exchange, late release");
   // NWM math warps + the producer + NRED reducer warps = NWT warps
   constexpr int NTC = NWM * 32;
   constexpr int NRED = NWT - NWM - 1;
   constexpr int NRW = NRED;
   static_assert(NRED >= 1, "no reducer warp");
   constexpr int NWC = NTC / 32;
-  constexpr int NSLOT = LL + 1;
+  constexpr int NSLOT = LL + 1 + (EARLY ? 1 : 0);
   constexpr int PUBW = 0;  // the publishing math warp
   // packed FMAs (config 3: 5.43 -> 5.38 ms with LL = 2; with LL = 3 they cost registers: 5.48 -> 5.60)
   constexpr bool F2 = SYSCD_GRID_F2 == 1 || (SYSCD_GRID_F2 == 2 && NWM == 6 && LL == 2 && BB == 1);
@@ -650,6 +661,155 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
         for (int b = 0; b < BB; ++b) dh[l][b] = 0.f;
 #define XS_OLD(l) ((i + NSLOT - (l)) % NSLOT)
 #define XS_RES ((i + NSLOT - LL) % NSLOT)
+      if constexpr (EARLY) {
+#if SYSCD_GRID_FXP && SYSCD_GRID_LATE_RELEASE
+        // ---- early-staging loop (BB = 1, packed FMAs).  Block e lives in slot
+        // e % NSLOT with NSLOT = LL + 2.  Iteration e:
+        //   1. resolve block c = e - LL - 1 (totals of event c) and add its step to w
+        //   2. s_e = x_e . w, reduce it with the cross terms accumulated earlier, publish
+        //   3. copy column e + 1 into the slot block c just left and accumulate its
+        //      cross terms x_{e+1} . x_{e+1-l}, l = 1..LL (no w involved), release its stage
+        float pg[LL > 0 ? LL : 1];  // cross terms of the block published next
+        static_assert(LL == 2, "early staging: LL = 2");
+        auto stage_next = [&](float (&xn)[RR], const float (&xa)[RR], const float (&xb)[RR]) {
+          mbar_wait(&full[stage], phase);
+          const float* x = ring + (size_t)stage * CTA_ROWS + tid;
+#pragma unroll
+          for (int r = 0; r < RR; ++r) xn[r] = x[r * NTC];
+          uint64_t* bar = &empty[stage];
+          if (++stage == (uint32_t)S) {
+            stage = 0;
+            phase ^= 1u;
+          }
+          unsigned long long ga = 0ull, gb = 0ull;
+#pragma unroll
+          for (int r = 0; r < RR; r += 2) {
+            const unsigned long long xv = pack2(xn[r], xn[r + 1]);
+            ga = ffma2(xv, pack2(xa[r], xa[r + 1]), ga);
+            gb = ffma2(xv, pack2(xb[r], xb[r + 1]), gb);
+          }
+          float lo, hi;
+          unpack2(ga, lo, hi);
+          pg[0] = lo + hi;
+          unpack2(gb, lo, hi);
+          pg[1] = lo + hi;
+          // every loaded register has been consumed by an FMA: release the stage
+          __syncwarp();
+          if (lane == 0)
+            asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];  // after %1"
+                         ::"r"(smem_addr(bar)), "f"(pg[0]) : "memory");
+        };
+        stage_next(xr[0][0], xr[NSLOT - 1][0], xr[NSLOT - 2][0]);
+        for (int e0 = 0; e0 < nb + LL + 1; e0 += NSLOT) {
+#pragma unroll
+          for (int i = 0; i < NSLOT; ++i) {
+            const int e = e0 + i;
+            if (e < nb + LL + 1) {
+              const int SR = (i + 1) % NSLOT;  // slot of block e - LL - 1, then of block e + 1
+              if (e >= LL + 1) {
+                // ---- 1. resolve block c
+                const int c = e - LL - 1;
+                const int64_t cpub = ebase + c;
+                mbar_wait(&totbar[cpub % kGTot], (uint32_t)((cpub / kGTot) & 1));
+                const float* t = tot + (cpub % kGTot) * kGVal;
+                float lin = t[0] * invS[SR];
+#pragma unroll
+                for (int l = 1; l <= LL; ++l) lin = fmaf(aG * dh[l - 1][0], t[l], lin);
+                const int4 mt = meta[(col0 + c) & (kGMeta - 1)];
+                const int j = mt.x;
+                float aj = __int_as_float(mt.y);
+                const float qj = __int_as_float(mt.z);
+                if (IID) {
+                  const int2 r0 = rcnt_ring[(rcnt - 1 - lane) & (kGRecent - 1)];
+                  const int2 r1 = rcnt_ring[(rcnt - 33 - lane) & (kGRecent - 1)];
+                  const unsigned m0 = __ballot_sync(0xffffffffu, r0.x == j);
+                  const unsigned m1 = __ballot_sync(0xffffffffu, r1.x == j);
+                  if (m0 | m1) {
+                    const int kk = m0 ? __ffs(m0) - 1 : 32 + __ffs(m1) - 1;
+                    aj = __int_as_float(rcnt_ring[(rcnt - 1 - kk) & (kGRecent - 1)].y);
+                  }
+                }
+                float an;
+                if (KIND == SYSCD_LOGISTIC_DUAL) {
+                  an = (float)coord_step(SYSCD_LOGISTIC_DUAL, (double)lin, A.a_d, (double)qj, A.lam,
+                                         (double)aj, A.n_coords);
+                } else {
+                  an = coord_step_fr(KIND, lin, __int_as_float(mt.w), A.lam_f, aj, A.inv_n_f);
+                }
+                float dc = 0.f;
+                if (isfinite(an)) {
+                  dc = an - aj;
+                  const float tq = a * dc;
+                  w2 = fmaf(tq, fmaf(tq, qj, lin + lin), w2);
+                  w2max = fmaxf(w2max, w2);
+                  if (cta == 0 && tid == 0) __stcg(A.alpha + j, an);
+                } else if (cta == 0 && tid == 0) {
+                  atomicOr(A.status, SYSCD_ENONFINITE);
+                }
+                if (IID) {
+                  __syncwarp();
+                  if (lane == 0) rcnt_ring[rcnt & (kGRecent - 1)] = make_int2(j, __float_as_int(aj + dc));
+                  __syncwarp();
+                  ++rcnt;
+                }
+#pragma unroll
+                for (int l = LL - 1; l > 0; --l) dh[l][0] = dh[l - 1][0];
+                dh[0][0] = dc;
+                const float sd = a * dc;
+                const unsigned long long sd2 = pack2(sd, sd);
+#pragma unroll
+                for (int r = 0; r < RR; r += 2) {
+                  const unsigned long long wn =
+                      ffma2(sd2, pack2(xr[SR][0][r], xr[SR][0][r + 1]), pack2(w[r], w[r + 1]));
+                  unpack2(wn, w[r], w[r + 1]);
+                }
+              }
+              if (e < nb) {
+                // ---- 2. s_e with the updated w, reduce, publish
+                unsigned long long s2 = 0ull;
+#pragma unroll
+                for (int r = 0; r < RR; r += 2)
+                  s2 = ffma2(pack2(xr[i][0][r], xr[i][0][r + 1]), pack2(w[r], w[r + 1]), s2);
+                float pv[NP];
+                {
+                  float lo, hi;
+                  unpack2(s2, lo, hi);
+                  pv[0] = lo + hi;
+                }
+#pragma unroll
+                for (int k = 1; k < NP; ++k) pv[k] = k < NS ? pg[k - 1] : 0.f;
+                const int64_t pub = ebase + e;
+                float* rslot = red + (size_t)(pub % kGRed) * 16 * NS;
+                const float tv = warp_sum_multi<NP>(pv, lane);
+                {
+                  const int idx = multi_index<NP>(lane);
+                  if ((lane & (32 / NP - 1)) == 0 && idx < NS) rslot[warp * NS + idx] = tv;
+                }
+                named_bar_sync(1, NTC);
+                invS[i] = __int_as_float((127 - 52 + ((c0_b + (__float_as_int(w2max) >> 23)) >> 1)) << 23);
+                if (warp == PUBW && lane < NS) {
+                  float v = 0.f;
+                  for (int q = 0; q < NWC; ++q) v += rslot[q * NS + lane];
+                  const float sc =
+                      lane < BB ? __int_as_float(0x7F000000 - __float_as_int(invS[i])) : scaleG;
+                  float f = v * sc;
+                  if (!(fabsf(f) < 1.8014399e16f)) {  // 2^54: NaN/Inf or bounds violated (bad sq)
+                    atomicOr(A.status, SYSCD_ENONFINITE);
+                    f = 0.f;
+                  }
+                  red_add_u64(A.recs + (size_t)(pub % kGNB) * kGSlotWords + lane,
+                              ((unsigned long long)__float2ll_rn(f) << 8) + 1ull);
+                }
+              }
+              if (e + 1 < nb) {
+                // ---- 3. column e + 1 and its cross terms (slots of blocks e, e-1, ...)
+                stage_next(xr[SR][0], xr[i][0], xr[(i + NSLOT - 1) % NSLOT][0]);
+              }
+            }
+          }
+        }
+#endif
+      } else
       for (int e0 = 0; e0 < nb + LL; e0 += NSLOT) {
 #pragma unroll
         for (int i = 0; i < NSLOT; ++i) {
@@ -1044,19 +1204,19 @@ struct GridEntry {
   const void* fn[4][2];  // [ridge / primal logistic, lasso, svm dual, logistic dual][iid]
 };
 
-template <int RR, int BB, int LL, int NWM, int NWT, int KIND>
+template <int RR, int BB, int LL, int NWM, int NWT, bool EARLY, int KIND>
 static void grid_fill(GridEntry& g, int k) {
-  g.fn[k][0] = (const void*)&k_grid_epoch<RR, BB, LL, KIND, false, NWM, NWT>;
-  g.fn[k][1] = (const void*)&k_grid_epoch<RR, BB, LL, KIND, true, NWM, NWT>;
+  g.fn[k][0] = (const void*)&k_grid_epoch<RR, BB, LL, KIND, false, NWM, NWT, EARLY>;
+  g.fn[k][1] = (const void*)&k_grid_epoch<RR, BB, LL, KIND, true, NWM, NWT, EARLY>;
 }
 
-template <int RR, int BB, int LL, int NWM = 13, int NWT = 16>
+template <int RR, int BB, int LL, int NWM = 13, int NWT = 16, bool EARLY = false>
 static GridEntry make_grid() {
   GridEntry g{RR, BB, LL, GridLayout<BB, LL>::kNS, NWM * 32, NWT * 32, {}};
-  grid_fill<RR, BB, LL, NWM, NWT, SYSCD_RIDGE>(g, 0);
-  grid_fill<RR, BB, LL, NWM, NWT, SYSCD_LASSO>(g, 1);
-  grid_fill<RR, BB, LL, NWM, NWT, SYSCD_SVM_DUAL>(g, 2);
-  grid_fill<RR, BB, LL, NWM, NWT, SYSCD_LOGISTIC_DUAL>(g, 3);
+  grid_fill<RR, BB, LL, NWM, NWT, EARLY, SYSCD_RIDGE>(g, 0);
+  grid_fill<RR, BB, LL, NWM, NWT, EARLY, SYSCD_LASSO>(g, 1);
+  grid_fill<RR, BB, LL, NWM, NWT, EARLY, SYSCD_SVM_DUAL>(g, 2);
+  grid_fill<RR, BB, LL, NWM, NWT, EARLY, SYSCD_LOGISTIC_DUAL>(g, 3);
   return g;
 }
 
@@ -1079,9 +1239,13 @@ static GridEntry g_grid_table[] = {
     // <36,1,4,6/8> 7.44 ms (255 registers); fewer, longer slices
     // <38,1,3,6/8> (138 CTAs) 5.92, <40,...> (131) 5.99, <43,1,3,5/7> 6.39.
     // With the fixed-point exchange the totals arrive early enough for
-    // LL = 2 (one FMA per row less, room for packed FMAs): 5.38 against 5.48
-    // ms.  LL = 3 stays reachable (SYSCD_GRID_CFG=5): it is bound by the
-    // CTA's own work per event, LL = 2 by the exchange chain.
+    // LL = 2 (one FMA per row less, room for packed FMAs), and that instance is
+    // bound by the exchange chain, so the early-staging loop (only the s-term
+    // FMAs between totals and publication) is the one selected: config 3 at
+    // 5.21 ms against 5.28 (LL = 2 without it) and 5.48 (LL = 3, bound by the
+    // CTA's own work per event).  The other two stay reachable through
+    // SYSCD_GRID_CFG=5 / 6 (ties go to the earlier entry).
+    make_grid<36, 1, 2, 6, 8, true>(),
     make_grid<36, 1, 2, 6, 8>(),
     make_grid<36, 1, 3, 6, 8>(),
 };

@@ -56,7 +56,11 @@ __global__ void k_sync(unsigned long long* recs, int E, int L, int sleep_ns, uns
         }
       __syncwarp();
       if (lane < NS) {
-        if (MODE >= 5) {
+        if (MODE >= 7) {
+          constexpr int M = MODE == 7 ? 4 : 8;
+          const unsigned long long fx = (unsigned long long)(long long)(cta - 70 + lane + e);
+          red_add_u64(recs + ((size_t)(e % NB) * M + cta % M) * 32 + lane, (fx << 8) + 1ull);
+        } else if (MODE >= 5) {
           const size_t stride = MODE == 6 ? 32 : 1;  // words between an event's values
           const unsigned long long fx = (unsigned long long)(long long)(cta - 70 + lane + e);
           red_add_u64(recs + ((size_t)(e % NB) * NS + lane) * stride * (MODE == 6 ? 1 : 1) +
@@ -67,6 +71,48 @@ __global__ void k_sync(unsigned long long* recs, int E, int L, int sleep_ns, uns
           st_rel(recs + ((size_t)(e % NB) * G + cta) * NS + lane, w);
         }
       }
+    }
+  } else if (MODE >= 7) {
+    // M sub-accumulators per event (CTA c adds into sub c % M, each on its own
+    // 256-byte line): fewer same-address atomics in a row; lane (m, c) polls
+    // word c of sub m, one event per load instruction, D events per pass
+    constexpr int M = MODE == 7 ? 4 : 8;
+    constexpr int D = 4;
+    __shared__ unsigned long long prev[NB][M * NS];
+    for (int i = lane; i < NB * M * NS; i += 32) (&prev[0][0])[i] = 0ull;
+    __syncwarp();
+    const int c = lane % NS, m = lane / NS;
+    const bool act = m < M;
+    const unsigned long long cnt = act ? (unsigned long long)((G - m + M - 1) / M) : 0ull;
+    int r0 = 0;
+    while (r0 < E) {
+      unsigned long long cur[D];
+      bool ok[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const int r = r0 + k;
+        cur[k] = 0ull;
+        if (act && r < E) cur[k] = ld_rel(recs + ((size_t)(r % NB) * M + m) * 32 + c);
+      }
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const int r = r0 + k;
+        ok[k] = !act || r >= E || ((cur[k] - prev[r % NB][lane]) & 0xFFull) == cnt;
+      }
+      int nd = 0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const bool all = __all_sync(0xffffffffu, ok[k]);
+        if (all && nd == k && r0 + k < E) {
+          if (act) prev[(r0 + k) % NB][lane] = cur[k];
+          ++nd;
+        }
+      }
+      __syncwarp();
+      if (lane == 0)
+        for (int q = 0; q < nd; ++q) fin[(r0 + q) % NB] = r0 + q + 1;
+      r0 += nd;
+      if (nd == 0 && sleep_ns > 0) __nanosleep(sleep_ns);
     }
   } else if (MODE >= 5) {
     // accumulator poller: lane l watches word l % NS of event r0 + l / NS
@@ -246,11 +292,11 @@ int main(int argc, char** argv) {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  const int Gs[] = {145, 148};
+  const int Gs[] = {145};
   const int Ls[] = {1, 2, 3};
-  const int sleeps[] = {0, 64, 256};
+  const int sleeps[] = {0, 32};
   printf("mode(events in flight) G L sleep_ns us_per_event\n");
-  for (int mode : {1, 2, 5, 6})
+  for (int mode : {5, 7, 8})
   for (int G : Gs) {
     if (G > sms) continue;
     for (int L : Ls)
@@ -265,7 +311,8 @@ int main(int argc, char** argv) {
         cudaEventRecord(a);
         void* fn = mode == 0 ? (void*)k_sync<0> : mode == 1 ? (void*)k_sync<1>
                  : mode == 2 ? (void*)k_sync<2> : mode == 4 ? (void*)k_sync<4>
-                 : mode == 5 ? (void*)k_sync<5> : mode == 6 ? (void*)k_sync<6> : (void*)k_sync<3>;
+                 : mode == 5 ? (void*)k_sync<5> : mode == 6 ? (void*)k_sync<6>
+                 : mode == 7 ? (void*)k_sync<7> : mode == 8 ? (void*)k_sync<8> : (void*)k_sync<3>;
         cudaLaunchCooperativeKernel(fn, dim3(G), dim3(64), args, 0, 0);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
