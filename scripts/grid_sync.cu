@@ -56,10 +56,14 @@ __global__ void k_sync(unsigned long long* recs, int E, int L, int sleep_ns, uns
         }
       __syncwarp();
       if (lane < NS) {
-        if (MODE >= 7) {
+        if (MODE == 7 || MODE == 8) {
           constexpr int M = MODE == 7 ? 4 : 8;
           const unsigned long long fx = (unsigned long long)(long long)(cta - 70 + lane + e);
           red_add_u64(recs + ((size_t)(e % NB) * M + cta % M) * 32 + lane, (fx << 8) + 1ull);
+        } else if (MODE == 9) {
+          const unsigned long long fx = (unsigned long long)(long long)(cta - 70 + lane + e);
+          for (int rep = 0; rep < 6; ++rep)
+            red_add_u64(recs + (size_t)(e % NB) * 32 + lane, (fx << 10) + 1ull);
         } else if (MODE >= 5) {
           const size_t stride = MODE == 6 ? 32 : 1;  // words between an event's values
           const unsigned long long fx = (unsigned long long)(long long)(cta - 70 + lane + e);
@@ -71,6 +75,33 @@ __global__ void k_sync(unsigned long long* recs, int E, int L, int sleep_ns, uns
           st_rel(recs + ((size_t)(e % NB) * G + cta) * NS + lane, w);
         }
       }
+    }
+  } else if (MODE == 9) {
+    // per-warp publication: 6 G contributions per word, 10-bit count
+    __shared__ unsigned long long prev9[NB][NS];
+    if (lane < NS)
+      for (int s = 0; s < NB; ++s) prev9[s][lane] = 0ull;
+    __syncwarp();
+    const int c = lane % NS, k = lane / NS;
+    constexpr int D = 4;
+    int r0 = 0;
+    while (r0 < E) {
+      const int r = r0 + k;
+      bool ok = true;
+      unsigned long long cur = 0;
+      if (k < D && r < E) {
+        cur = ld_rel(recs + (size_t)(r % NB) * 32 + c);
+        ok = ((cur - prev9[r % NB][c]) & 0x3FFull) == (unsigned long long)((6 * G) & 0x3FF);
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, ok);
+      int nd = 0;
+      while (nd < D && r0 + nd < E && ((m >> (nd * NS)) & ((1u << NS) - 1)) == ((1u << NS) - 1)) ++nd;
+      if (k < nd) prev9[r % NB][c] = cur;
+      __syncwarp();
+      if (lane == 0)
+        for (int q = 0; q < nd; ++q) fin[(r0 + q) % NB] = r0 + q + 1;
+      r0 += nd;
+      if (nd == 0 && sleep_ns > 0) __nanosleep(sleep_ns);
     }
   } else if (MODE >= 7) {
     // M sub-accumulators per event (CTA c adds into sub c % M, each on its own
@@ -296,7 +327,7 @@ int main(int argc, char** argv) {
   const int Ls[] = {1, 2, 3};
   const int sleeps[] = {0, 32};
   printf("mode(events in flight) G L sleep_ns us_per_event\n");
-  for (int mode : {5, 7, 8})
+  for (int mode : {5, 9})
   for (int G : Gs) {
     if (G > sms) continue;
     for (int L : Ls)
@@ -312,7 +343,8 @@ int main(int argc, char** argv) {
         void* fn = mode == 0 ? (void*)k_sync<0> : mode == 1 ? (void*)k_sync<1>
                  : mode == 2 ? (void*)k_sync<2> : mode == 4 ? (void*)k_sync<4>
                  : mode == 5 ? (void*)k_sync<5> : mode == 6 ? (void*)k_sync<6>
-                 : mode == 7 ? (void*)k_sync<7> : mode == 8 ? (void*)k_sync<8> : (void*)k_sync<3>;
+                 : mode == 7 ? (void*)k_sync<7> : mode == 8 ? (void*)k_sync<8>
+                 : mode == 9 ? (void*)k_sync<9> : (void*)k_sync<3>;
         cudaLaunchCooperativeKernel(fn, dim3(G), dim3(64), args, 0, 0);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
