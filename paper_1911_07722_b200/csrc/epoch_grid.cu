@@ -65,13 +65,14 @@ constexpr int kGRed = 8;      // CTA-reduction slots (events)
 // across 145 CTAs: 1.55-1.8 us against 2.9-3.1 us, scripts/grid_sync.cu, and
 // no poll traffic competing with the A stream).  The shifts are powers of two
 // derived from Cauchy-Schwarz bounds every CTA computes identically:
-//   Gram words   |x_i . x_k| <= max_j q_j                    (fixed per launch)
-//   s words      |x_e . w|  <= sqrt(max_j q_j) ||w||, with ||w||^2 tracked
-//                exactly from the resolved steps (||w + t x||^2 = ||w||^2 +
-//                t (2 x.w + t q)), starting from d max_i |u_i|^2.
-// The sums over CTAs obey the same bounds, so 55 bits never overflow; the
-// resolution is >= 2^-52 of the bound, far below the fp32 rounding of the
-// partials themselves.  SYSCD_GRID_FXP=0 builds the tagged-float records.
+//   Gram words   |x_e . x_k| <= sqrt(q_e max_j q_j)
+//   s words      |x_e . w|  <= sqrt(q_e) ||w||, with ||w||^2 tracked exactly
+//                from the resolved steps (||w + t x||^2 = ||w||^2 + t (2 x.w +
+//                t q)), starting from d max_i |u_i|^2.
+// (q_e: the event's own column norm, so columns of very different scale keep
+// their relative precision.)  The sums over CTAs obey the same bounds, so 55
+// bits never overflow; the resolution is >= 2^-52 of the bound, far below the
+// fp32 rounding of the partials themselves.  SYSCD_GRID_FXP=0 builds the tagged-float records.
 #ifndef SYSCD_GRID_FXP
 #define SYSCD_GRID_FXP 1
 #endif
@@ -193,6 +194,23 @@ __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
+}
+
+// Biased exponent of a non-negative float, floored at 2^-60 (zero columns,
+// w = 0): keeps every shift below in the normal range.
+__device__ __forceinline__ int fexp60(float v) {
+  const int e = __float_as_int(v) >> 23;
+  return e < 67 ? 67 : e;
+}
+// 2^-shift for a value bounded by sqrt(A B), A < 2^(ea-126), B < 2^(eb-126)
+// (ea, eb biased exponents): shift = 52 - ceil(log2 of the bound), so the
+// scaled value stays below 2^52.  Publisher and decoders evaluate this same
+// integer expression on the same bits.
+__device__ __forceinline__ float inv_scale(int ea, int eb) {
+  return __int_as_float((127 - 52 + ((ea + eb - 251) >> 1)) << 23);
+}
+__device__ __forceinline__ float recip_pow2(float p) {  // 1/p for a normal power of two
+  return __int_as_float(0x7F000000 - __float_as_int(p));
 }
 
 // 2^sh as a float (sh clamped to the normal range) and the power-of-two pair
@@ -392,12 +410,12 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
     w2_init = fmaxf((float)d * wg * wg, 8.6736174e-19f);
     __syncthreads();  // scr is the CTA-reduction ring from here on
   }
-  // Gram words: |g| <= qmax < 2^(eq+1)  ->  |g| 2^shG < 2^52
-  const int eq_b = (__float_as_int(qmax_b) >> 23) - 127;
-  const float invG = pow2f(eq_b + 1 - 52);
-  // s words: |s| <= sqrt(qmax W) < 2^((eq + ew + 3) >> 1) with ew the unbiased
-  // exponent of W  ->  shS = 52 - ((eq + ew + 3) >> 1); c0 folds the bias
-  const int c0_b = eq_b + 3 - 127;
+  // Scales (per event, from bounds every CTA evaluates identically):
+  //   s words     |x_e . w|   <= sqrt(q_e ||w||^2)   (||w||^2: running maximum, tracked)
+  //   Gram words  |x_e . x_k| <= sqrt(q_e q_max)
+  // both relative to the event's own column norm, so badly scaled columns
+  // (norms apart by many orders of magnitude) keep their relative precision.
+  const int eqm = fexp60(qmax_b);
 #endif
 
   // ------------------------------------------------------------ reducer state
@@ -629,13 +647,25 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
     const float inv_a = (float)(1.0 / A.a_d);
 #if SYSCD_GRID_FXP
     float w2 = w2_init, w2max = w2_init;  // ||w||^2 (tracked) and its running maximum
-    float invS[NSLOT];                     // 2^-shS of the event in each register slot
+    int ewr[NSLOT];  // exponent of the ||w||^2 bound the event in each register slot was scaled with
 #pragma unroll
-    for (int sl = 0; sl < NSLOT; ++sl) invS[sl] = 1.f;
-    const float aG = a * invG;  // Gram totals are decoded inside the step's a * delta factor
-    const float scaleG = __int_as_float(0x7F000000 - __float_as_int(invG));
-#else
-    const float aG = a;
+    for (int sl = 0; sl < NSLOT; ++sl) ewr[sl] = 127;
+    // column (within the event) whose norm scales the publisher lane's word
+    int pub_b = 0;
+    if (lane < NS) {
+      if (lane < BB) {
+        pub_b = lane;
+      } else if (lane < Lay::kX) {
+        int idx = lane - BB, bb = 1;
+        while (idx >= bb) {
+          idx -= bb;
+          ++bb;
+        }
+        pub_b = bb;
+      } else {
+        pub_b = ((lane - Lay::kX) / BB) % BB;
+      }
+    }
 #endif
     uint32_t stage = 0, phase = 0;
 #ifdef SYSCD_GRID_CLK
@@ -712,13 +742,15 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
                 const int64_t cpub = ebase + c;
                 mbar_wait(&totbar[cpub % kGTot], (uint32_t)((cpub / kGTot) & 1));
                 const float* t = tot + (cpub % kGTot) * kGVal;
-                float lin = t[0] * invS[SR];
-#pragma unroll
-                for (int l = 1; l <= LL; ++l) lin = fmaf(aG * dh[l - 1][0], t[l], lin);
                 const int4 mt = meta[(col0 + c) & (kGMeta - 1)];
                 const int j = mt.x;
                 float aj = __int_as_float(mt.y);
                 const float qj = __int_as_float(mt.z);
+                const int eqj = fexp60(qj);
+                const float aG = a * inv_scale(eqj, eqm);
+                float lin = t[0] * inv_scale(eqj, ewr[SR]);
+#pragma unroll
+                for (int l = 1; l <= LL; ++l) lin = fmaf(aG * dh[l - 1][0], t[l], lin);
                 if (IID) {
                   const int2 r0 = rcnt_ring[(rcnt - 1 - lane) & (kGRecent - 1)];
                   const int2 r1 = rcnt_ring[(rcnt - 33 - lane) & (kGRecent - 1)];
@@ -785,13 +817,13 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
                   const int idx = multi_index<NP>(lane);
                   if ((lane & (32 / NP - 1)) == 0 && idx < NS) rslot[warp * NS + idx] = tv;
                 }
+                ewr[i] = __float_as_int(w2max) >> 23;
+                const int eqe = fexp60(__int_as_float(meta[(col0 + e) & (kGMeta - 1)].z));
                 named_bar_sync(1, NTC);
-                invS[i] = __int_as_float((127 - 52 + ((c0_b + (__float_as_int(w2max) >> 23)) >> 1)) << 23);
                 if (warp == PUBW && lane < NS) {
                   float v = 0.f;
                   for (int q = 0; q < NWC; ++q) v += rslot[q * NS + lane];
-                  const float sc =
-                      lane < BB ? __int_as_float(0x7F000000 - __float_as_int(invS[i])) : scaleG;
+                  const float sc = recip_pow2(inv_scale(eqe, lane < BB ? ewr[i] : eqm));
                   float f = v * sc;
                   if (!(fabsf(f) < 1.8014399e16f)) {  // 2^54: NaN/Inf or bounds violated (bad sq)
                     atomicOr(A.status, SYSCD_ENONFINITE);
@@ -1014,16 +1046,17 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
                 A.dbg[8192 + pub * 160 + cta] = gtimer_g();
 #endif
 #if SYSCD_GRID_FXP
-              // this event's s-scale from the running bound on ||w||^2 (the w of
-              // the partials above: every step resolved so far is tracked)
-              invS[i] = __int_as_float((127 - 52 + ((c0_b + (__float_as_int(w2max) >> 23)) >> 1)) << 23);
+              // this event's s-scale comes from the running bound on ||w||^2 (the w
+              // of the partials above: every step resolved so far is tracked)
+              ewr[i] = __float_as_int(w2max) >> 23;
 #endif
               if (warp == PUBW && lane < NS) {
                 float v = 0.f;
                 for (int q = 0; q < NWC; ++q) v += rslot[q * NS + lane];
 #if SYSCD_GRID_FXP
-                const float sc =
-                    lane < BB ? __int_as_float(0x7F000000 - __float_as_int(invS[i])) : scaleG;
+                const int eqe = fexp60(
+                    __int_as_float(meta[(col0 + min(e * BB + pub_b, m - 1)) & (kGMeta - 1)].z));
+                const float sc = recip_pow2(inv_scale(eqe, lane < BB ? ewr[i] : eqm));
                 float f = v * sc;
                 if (!(fabsf(f) < 1.8014399e16f)) {  // 2^54: NaN/Inf or bounds violated (bad sq)
                   atomicOr(A.status, SYSCD_ENONFINITE);
@@ -1058,9 +1091,16 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
                 dcur[b] = 0.f;
                 const int col = c * BB + b;
                 if (col < m) {
+                  const int4 mt = meta[(col0 + col) & (kGMeta - 1)];
+                  const int j = mt.x;
+                  float aj = __int_as_float(mt.y);
+                  const float qj = __int_as_float(mt.z);
 #if SYSCD_GRID_FXP
-                  float lin = t[Lay::kS + b] * invS[XS_RES];
+                  const int eqj = fexp60(qj);
+                  const float aG = a * inv_scale(eqj, eqm);  // Gram totals decode inside a * delta
+                  float lin = t[Lay::kS + b] * inv_scale(eqj, ewr[XS_RES]);
 #else
+                  const float aG = a;
                   float lin = t[Lay::kS + b];
 #endif
 #pragma unroll
@@ -1070,10 +1110,6 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
                       lin = fmaf(aG * dh[l - 1][k], t[Lay::gx(l, b, k)], lin);
 #pragma unroll
                   for (int k = 0; k < b; ++k) lin = fmaf(aG * dcur[k], t[Lay::gin(b, k)], lin);
-                  const int4 mt = meta[(col0 + col) & (kGMeta - 1)];
-                  const int j = mt.x;
-                  float aj = __int_as_float(mt.y);
-                  const float qj = __int_as_float(mt.z);
                   if (IID) {
                     const int2 r0 = rcnt_ring[(rcnt - 1 - lane) & (kGRecent - 1)];
                     const int2 r1 = rcnt_ring[(rcnt - 33 - lane) & (kGRecent - 1)];

@@ -241,7 +241,7 @@ def test_sparse_metrics_rows_and_lazy_rounds(cuda):
         assert m.rel_change == ref.rel_change
 
 
-def _edge_pair(kind, d, n, seed, zero_cols=(), lam=None):
+def _edge_pair(kind, d, n, seed, zero_cols=(), lam=None, col_scale=None, zero_y=False):
     """The same tiny problem for the GPU mirror and the oracle (dense store)."""
     from paper_1911_07722_b200 import (COORDINATES_ARE_EXAMPLES, COORDINATES_ARE_FEATURES,
                                        ColumnMatrix, GlmProblem, LabeledDataset, SmoothLoss)
@@ -249,8 +249,10 @@ def _edge_pair(kind, d, n, seed, zero_cols=(), lam=None):
     A = g.standard_normal((d, n)).astype(np.float32)
     for j in zero_cols:
         A[:, j] = 0.0
+    if col_scale is not None:
+        A = (A * np.asarray(col_scale, dtype=np.float32)[None, :]).astype(np.float32)
     if kind in ("ridge", "lasso"):
-        y = g.standard_normal(d)
+        y = np.zeros(d) if zero_y else g.standard_normal(d)
         lam = lam or (0.5 if kind == "ridge" else 0.05 * float(np.abs(A.T @ y).max()))
         ds = LabeledDataset(ColumnMatrix(d, n, dense=A), y, COORDINATES_ARE_FEATURES)
         pb = GlmProblem.build(ds, SmoothLoss.squared_error(), lam,
@@ -291,6 +293,51 @@ def test_edge_geometries(cuda, kind, d, n, kw):
         assert np.all(res.alpha >= 0) and np.all(res.alpha <= 1)
     if n > 2 and kind in ("ridge", "lasso"):
         assert res.alpha[0] == 0.0  # an all-zero column never moves
+
+
+@pytest.mark.parametrize("kind", ["ridge", "lasso", "svm_dual"])
+@pytest.mark.parametrize("sampling", ["perm", "iid"])
+def test_grid_fixed_point_scales(cuda, kind, sampling):
+    """The grid kernel sums its partials in fixed point with scales from
+    Cauchy-Schwarz bounds relative to each column's own norm: columns whose
+    norms lie six orders of magnitude apart (q apart by 1e12) keep the
+    trajectory parity of well-scaled data."""
+    from paper_1911_07722_b200 import SolverConfig, run_syscd
+    d, n = 60013, 24
+    scale = 10.0 ** ((np.arange(n) % 7) - 3.0)  # 1e-3 .. 1e3
+    kw = dict(K=1, P=1, bucket_size=4)
+    if sampling == "iid":
+        kw.update(sampling="iid", T3=3, T4=5)
+    pb, ob = _edge_pair(kind, d, n, seed=977, col_scale=scale, lam=0.5 if kind != "svm_dual" else None)
+    res = run_syscd(pb, SolverConfig(seed=3, T1=4, **kw))
+    ores = O.run_syscd(ob, O.OracleConfig(seed=3, T1=4, **kw))
+    assert_parity(res, ores)
+
+
+def test_grid_fixed_point_zero_gradient(cuda):
+    """y = 0 and alpha = 0: the shared vector and every partial are exactly
+    zero (the bound on ||w|| is zero too): nothing moves and nothing is
+    flagged."""
+    from paper_1911_07722_b200 import SolverConfig, run_syscd
+    pb, _ = _edge_pair("ridge", 60013, 24, seed=5, zero_y=True)
+    res = run_syscd(pb, SolverConfig(K=1, P=1, bucket_size=4, seed=3, T1=2))
+    assert np.array_equal(res.alpha, np.zeros(24))
+    assert all(m.objective == 0.0 for m in res.metrics)
+
+
+def test_grid_fixed_point_non_finite_is_flagged(cuda):
+    """Partials that overflow fp32 in tall columns must surface as
+    NonFiniteUpdateError (the fixed-point conversion would otherwise swallow
+    the Inf)."""
+    from paper_1911_07722_b200 import (COORDINATES_ARE_FEATURES, ColumnMatrix, GlmProblem,
+                                       LabeledDataset, NonFiniteUpdateError, SmoothLoss,
+                                       SolverConfig, run_syscd)
+    d, n = 60013, 24
+    big = np.full((d, n), 3e38, dtype=np.float64)
+    ds = LabeledDataset(ColumnMatrix(d, n, dense=big), np.ones(d), COORDINATES_ARE_FEATURES)
+    pb = GlmProblem.build(ds, SmoothLoss.squared_error(), 0.5)
+    with pytest.raises(NonFiniteUpdateError):
+        run_syscd(pb, SolverConfig(K=1, P=1, bucket_size=4, seed=3, T1=2))
 
 
 def _sparse_edge_pair(kind, d, n, seed):
