@@ -587,12 +587,8 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
       bool have = false;
       const unsigned long long gcount = (unsigned long long)(G & 0xFF);
       if (rw > 0) r0 = events;  // one warp gathers every event (a sector per event)
-      while (r0 < events) {
-        if (act && !have && r_me < events && r_me <= r0 + LL + 1) {
-          cur = ld_tagged(A.recs + (size_t)(r_me % kGNB) * kGSlotWords + c);
-          have = ((cur - prevw[(r_me % kGNB) * NS + c]) & 0xFFull) == gcount;
-        }
-        unsigned m = __ballot_sync(0xffffffffu, have || !act);
+      // hand over, in order, the events whose group has every word complete
+      auto hand_over = [&](unsigned m) -> bool {
         bool prog = false;
         while (r0 < events) {
           const int g = (int)(r0 % D);
@@ -617,7 +613,14 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
           ++r0;
           prog = true;
         }
-        if (!prog) __nanosleep(SYSCD_GRID_SLEEP);
+        return prog;
+      };
+      while (r0 < events) {
+        if (act && !have && r_me < events && r_me <= r0 + LL + 1) {
+          cur = ld_tagged(A.recs + (size_t)(r_me % kGNB) * kGSlotWords + c);
+          have = ((cur - prevw[(r_me % kGNB) * NS + c]) & 0xFFull) == gcount;
+        }
+        if (!hand_over(__ballot_sync(0xffffffffu, have || !act))) __nanosleep(SYSCD_GRID_SLEEP);
       }
 #else
       for (;;) {

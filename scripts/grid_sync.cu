@@ -64,6 +64,9 @@ __global__ void k_sync(unsigned long long* recs, int E, int L, int sleep_ns, uns
           const unsigned long long fx = (unsigned long long)(long long)(cta - 70 + lane + e);
           for (int rep = 0; rep < 6; ++rep)
             red_add_u64(recs + (size_t)(e % NB) * 32 + lane, (fx << 10) + 1ull);
+        } else if (MODE == 10) {
+          const unsigned long long fx = (unsigned long long)(long long)(cta - 70 + lane + e);
+          red_add_u64(recs + (size_t)(e % NB) * 32 + lane, (fx << 8) + 1ull);
         } else if (MODE >= 5) {
           const size_t stride = MODE == 6 ? 32 : 1;  // words between an event's values
           const unsigned long long fx = (unsigned long long)(long long)(cta - 70 + lane + e);
@@ -74,6 +77,57 @@ __global__ void k_sync(unsigned long long* recs, int E, int L, int sleep_ns, uns
           const unsigned long long w = ((unsigned long long)(e + 1) << 32) | (unsigned)(cta + lane);
           st_rel(recs + ((size_t)(e % NB) * G + cta) * NS + lane, w);
         }
+      }
+    }
+  } else if (MODE == 10) {
+    // mode 5 with PIPELINED polls: a new poll of every in-flight event is
+    // issued every sleep_ns without waiting for the previous one to return
+    // (NF polls in flight), so a completed word is seen ~half a round trip
+    // after it lands instead of up to one and a half
+    constexpr int NF = 4;
+    __shared__ unsigned long long prevA[NB][NS];
+    if (lane < NS)
+      for (int s = 0; s < NB; ++s) prevA[s][lane] = 0ull;
+    __syncwarp();
+    const int c = lane % NS, k = lane / NS;
+    constexpr int D = 4;
+    int r0 = 0;
+    unsigned long long fl[NF];
+    int fr[NF];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      fl[f] = 0ull;
+      fr[f] = -1000;
+    }
+    while (r0 < E) {
+#pragma unroll
+      for (int f = 0; f < NF; ++f) {
+        // consume the oldest poll (slot f), then reissue it
+        const int r = fr[f] + k;
+        bool ok = true;
+        if (fr[f] >= 0 && k < D && r < E && r >= r0)
+          ok = ((fl[f] - prevA[r % NB][c]) & 0xFFull) == (unsigned long long)(G & 0xFF);
+        else if (fr[f] < 0 || r >= E)
+          ok = fr[f] >= 0 && r >= E;
+        // lanes whose event was already handed over (r < r0) count as complete
+        const unsigned m = __ballot_sync(0xffffffffu, ok);
+        int nd = 0;
+        if (fr[f] >= 0) {
+          const int sh = r0 - fr[f];  // groups already handed over since this poll was issued
+          while (sh + nd < D && r0 + nd < E &&
+                 ((m >> ((sh + nd) * NS)) & ((1u << NS) - 1)) == ((1u << NS) - 1))
+            ++nd;
+          if (k >= sh && k < sh + nd) prevA[r % NB][c] = fl[f];
+        }
+        __syncwarp();
+        if (lane == 0)
+          for (int q = 0; q < nd; ++q) fin[(r0 + q) % NB] = r0 + q + 1;
+        r0 += nd;
+        if (r0 >= E) break;
+        fr[f] = r0;
+        const int rn = r0 + k;
+        fl[f] = (k < D && rn < E) ? ld_rel(recs + (size_t)(rn % NB) * 32 + c) : 0ull;
+        if (sleep_ns > 0) __nanosleep(sleep_ns);
       }
     }
   } else if (MODE == 9) {
@@ -325,9 +379,9 @@ int main(int argc, char** argv) {
   cudaEventCreate(&b);
   const int Gs[] = {145};
   const int Ls[] = {1, 2, 3};
-  const int sleeps[] = {0, 32};
+  const int sleeps[] = {0, 32, 64, 128};
   printf("mode(events in flight) G L sleep_ns us_per_event\n");
-  for (int mode : {5, 9})
+  for (int mode : {5, 10})
   for (int G : Gs) {
     if (G > sms) continue;
     for (int L : Ls)
@@ -344,7 +398,7 @@ int main(int argc, char** argv) {
                  : mode == 2 ? (void*)k_sync<2> : mode == 4 ? (void*)k_sync<4>
                  : mode == 5 ? (void*)k_sync<5> : mode == 6 ? (void*)k_sync<6>
                  : mode == 7 ? (void*)k_sync<7> : mode == 8 ? (void*)k_sync<8>
-                 : mode == 9 ? (void*)k_sync<9> : (void*)k_sync<3>;
+                 : mode == 9 ? (void*)k_sync<9> : mode == 10 ? (void*)k_sync<10> : (void*)k_sync<3>;
         cudaLaunchCooperativeKernel(fn, dim3(G), dim3(64), args, 0, 0);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
