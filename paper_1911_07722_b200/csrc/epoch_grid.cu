@@ -1287,6 +1287,9 @@ static GridEntry g_grid_table[] = {
     make_grid<36, 1, 2, 6, 8, true>(),
     make_grid<36, 1, 2, 6, 8>(),
     make_grid<36, 1, 3, 6, 8>(),
+#ifdef SYSCD_GRID_EXPERIMENTS
+    make_grid<36, 2, 1, 6, 8>(),
+#endif
 };
 constexpr int kGridTable = sizeof(g_grid_table) / sizeof(g_grid_table[0]);
 
