@@ -1284,7 +1284,9 @@ static GridEntry g_grid_table[] = {
     // 5.21 ms against 5.28 (LL = 2 without it) and 5.48 (LL = 3, bound by the
     // CTA's own work per event).  The other two stay reachable through
     // SYSCD_GRID_CFG=5 / 6 (ties go to the earlier entry).
+#if SYSCD_GRID_FXP && SYSCD_GRID_LATE_RELEASE
     make_grid<36, 1, 2, 6, 8, true>(),
+#endif
     make_grid<36, 1, 2, 6, 8>(),
     make_grid<36, 1, 3, 6, 8>(),
 #ifdef SYSCD_GRID_EXPERIMENTS
