@@ -12,13 +12,19 @@
 // (value << 8) + 1 into the event's NS accumulator words with red.add.u64 (the
 // L2 sums; integer, so order-independent), the poller reads one 32-byte sector
 // and an event is complete when the low byte advanced by G (up to 8 events per
-// poll instruction); 6 the same with each word on its own 256-byte line.
+// poll instruction); 6 the same with each word on its own 256-byte line; 7 / 8
+// four / eight sub-accumulators per event; 9 six contributions per CTA
+// (per-warp publication); 10 pipelined polls (several loads of a word in
+// flight).  k_sync_cluster<CS>: clusters of CS CTAs pre-reduce through DSMEM,
+// only the leaders touch L2.  On a B200 the plain mode 5 is the fastest of all
+// (profiles/r2d_grid_sync_*.txt).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/grid_sync scripts/grid_sync.cu
 //   /tmp/grid_sync
 #include <cstdio>
 #include <cstdint>
 #include <cstdlib>
 #include <cuda_runtime.h>
+#include <cooperative_groups.h>
 
 constexpr int NS = 4;
 constexpr int NQ = 5;
@@ -367,6 +373,104 @@ __global__ void k_sync(unsigned long long* recs, int E, int L, int sleep_ns, uns
   }
 }
 
+// Hierarchical exchange: clusters of CS CTAs.  Members push their tagged
+// partial words into the leader's shared memory (DSMEM store, single-copy
+// atomic 64-bit words), the leader adds them to its own and contributes ONE
+// red.add.u64 per word; only the G / CS leaders poll L2, and forward "event
+// complete" to their members through DSMEM.  Fewer contributions and pollers
+// on the hot line, two DSMEM hops more on the chain.
+template <int CS>
+__global__ void k_sync_cluster(unsigned long long* recs, int E, int L, int sleep_ns,
+                               unsigned long long* t_out) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  __shared__ volatile int fin[NB];
+  __shared__ unsigned long long inbox[NB][CS][NS];
+  __shared__ unsigned long long totw[NB];
+  __shared__ unsigned long long prevc[NB][NS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x, cta = blockIdx.x, NL = G / CS;
+  for (int i = threadIdx.x; i < NB * CS * NS; i += blockDim.x) (&inbox[0][0][0])[i] = 0ull;
+  for (int i = threadIdx.x; i < NB * NS; i += blockDim.x) (&prevc[0][0])[i] = 0ull;
+  if (threadIdx.x < NB) {
+    fin[threadIdx.x] = 0;
+    totw[threadIdx.x] = 0ull;
+  }
+  cl.sync();
+  unsigned long long t0 = 0;
+  if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  if (warp == 0) {
+    for (int e = 0; e < E; ++e) {
+      if (lane == 0 && e - L - 1 >= 0)
+        while (fin[(e - L - 1) % NB] != e - L) {
+        }
+      __syncwarp();
+      if (lane < NS) {
+        const unsigned long long fx = (unsigned long long)(unsigned)(cta + lane + e) & 0xFFFFull;
+        if (rank == 0) {
+          unsigned long long sum = fx;
+          for (int m = 1; m < CS; ++m) {
+            volatile unsigned long long* p = &inbox[e % NB][m][lane];
+            unsigned long long w;
+            while ((unsigned)((w = *p) >> 32) != (unsigned)(e + 1)) {
+            }
+            sum += w & 0xFFFFFFFFull;
+          }
+          red_add_u64(recs + (size_t)(e % NB) * 32 + lane, (sum << 8) + 1ull);
+        } else {
+          unsigned long long* rp = cl.map_shared_rank(&inbox[e % NB][rank][lane], 0);
+          *(volatile unsigned long long*)rp = ((unsigned long long)(e + 1) << 32) | fx;
+        }
+      }
+    }
+  } else if (rank == 0) {
+    const int c = lane % NS, k = lane / NS;
+    constexpr int D = 4;
+    int r0 = 0;
+    while (r0 < E) {
+      const int r = r0 + k;
+      bool ok = true;
+      unsigned long long cur = 0;
+      if (k < D && r < E) {
+        cur = ld_rel(recs + (size_t)(r % NB) * 32 + c);
+        ok = ((cur - prevc[r % NB][c]) & 0xFFull) == (unsigned long long)(NL & 0xFF);
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, ok);
+      int nd = 0;
+      while (nd < D && r0 + nd < E && ((m >> (nd * NS)) & ((1u << NS) - 1)) == ((1u << NS) - 1)) ++nd;
+      if (k < nd) prevc[r % NB][c] = cur;
+      __syncwarp();
+      for (int q = 0; q < nd; ++q) {
+        if (lane >= 1 && lane < CS) {
+          unsigned long long* rp = cl.map_shared_rank(&totw[(r0 + q) % NB], lane);
+          *(volatile unsigned long long*)rp = (unsigned long long)(r0 + q + 1);
+        }
+        if (lane == 0) fin[(r0 + q) % NB] = r0 + q + 1;
+      }
+      r0 += nd;
+      if (nd == 0 && sleep_ns > 0) __nanosleep(sleep_ns);
+    }
+  } else {
+    for (int r = 0; r < E; ++r) {
+      if (lane == 0) {
+        volatile unsigned long long* p = &totw[r % NB];
+        while (*p != (unsigned long long)(r + 1)) {
+        }
+        fin[r % NB] = r + 1;
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    t_out[cta] = t1 - t0;
+  }
+  cl.sync();
+}
+
 int main(int argc, char** argv) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -377,11 +481,11 @@ int main(int argc, char** argv) {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  const int Gs[] = {145};
+  const int Gs[] = {144, 145};
   const int Ls[] = {1, 2, 3};
-  const int sleeps[] = {0, 32, 64, 128};
+  const int sleeps[] = {0, 32};
   printf("mode(events in flight) G L sleep_ns us_per_event\n");
-  for (int mode : {5, 10})
+  for (int mode : {5})
   for (int G : Gs) {
     if (G > sms) continue;
     for (int L : Ls)
@@ -405,6 +509,36 @@ int main(int argc, char** argv) {
         float ms = 0;
         cudaEventElapsedTime(&ms, a, b);
         printf("%d %d %d %d %.3f\n", mode, G, L, sl, ms * 1e3 / E);
+        fflush(stdout);
+      }
+  }
+  for (int cs : {2, 4}) {
+    const int G = 144;
+    for (int L : Ls)
+      for (int sl : {0, 32}) {
+        cudaMemset(recs, 0, ((size_t)NB * 160 * NS + NB) * 8);
+        int Ev = E, Lv = L, slv = sl;
+        void* args[] = {&recs, &Ev, &Lv, &slv, &tout};
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(G);
+        cfg.blockDim = dim3(64);
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        at[1].id = cudaLaunchAttributeCooperative;
+        at[1].val.cooperative = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 2;
+        const void* fn = cs == 2 ? (const void*)k_sync_cluster<2> : (const void*)k_sync_cluster<4>;
+        cudaEventRecord(a);
+        cudaError_t er = cudaLaunchKernelExC(&cfg, fn, args);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        printf("cluster%d %d %d %d %.3f %s\n", cs, G, L, sl, ms * 1e3 / E, cudaGetErrorString(er));
         fflush(stdout);
       }
   }
