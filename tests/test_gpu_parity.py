@@ -30,6 +30,10 @@ CASES = [
     (0, 0.05, dict(K=1, P=1, bucket_size=8, T1=5)),
     (0, 0.05, dict(K=1, P=2, bucket_size=4, T2=3, T1=4)),
     (0, 0.05, dict(K=2, P=2, bucket_size=4, T2=2, repartition="static", T1=4)),
+    # K_local = 2 with T2 = 3 (not a divisor of the plan batch): the node loop revisits
+    # earlier rounds, i.e. re-plans into a buffer the prefetch stream may still own
+    (0, 0.05, dict(K=2, P=2, bucket_size=4, T2=3, T1=5)),
+    (2, 0.01, dict(K=2, P=2, bucket_size=2, T2=3, T1=4)),
     (0, 0.05, dict(K=1, P=3, bucket_size=5, T3=2, T4=3, T1=4)),
     (0, 0.05, dict(K=1, P=2, bucket_size=4, sampling="iid", T3=2, T4=3, T1=4)),
     (0, 0.05, dict(K=1, P=5, bucket_size=1, T1=4)),
