@@ -13,7 +13,8 @@
 // L2 sums; integer, so order-independent), the poller reads one 32-byte sector
 // and an event is complete when the low byte advanced by G (up to 8 events per
 // poll instruction); 6 the same with each word on its own 256-byte line; 7 / 8
-// four / eight sub-accumulators per event; 9 six contributions per CTA
+// four / eight sub-accumulators per event (12 / 13: two / four in the slot's
+// own line); 9 six contributions per CTA
 // (per-warp publication); 10 pipelined polls (several loads of a word in
 // flight).  k_sync_cluster<CS>: clusters of CS CTAs pre-reduce through DSMEM,
 // only the leaders touch L2.  On a B200 the plain mode 5 is the fastest of all
@@ -62,10 +63,11 @@ __global__ void k_sync(unsigned long long* recs, int E, int L, int sleep_ns, uns
         }
       __syncwarp();
       if (lane < NS) {
-        if (MODE == 7 || MODE == 8) {
-          constexpr int M = MODE == 7 ? 4 : 8;
+        if (MODE == 7 || MODE == 8 || MODE == 12 || MODE == 13) {
+          constexpr int M = MODE == 7 ? 4 : MODE == 8 ? 8 : MODE == 12 ? 2 : 4;
+          constexpr int SUB = MODE >= 12 ? NS : 32;  // 12 / 13: the sub-accumulators share the slot's line
           const unsigned long long fx = (unsigned long long)(long long)(cta - 70 + lane + e);
-          red_add_u64(recs + ((size_t)(e % NB) * M + cta % M) * 32 + lane, (fx << 8) + 1ull);
+          red_add_u64(recs + (size_t)(e % NB) * 8 * 32 + (size_t)(cta % M) * SUB + lane, (fx << 8) + 1ull);
         } else if (MODE == 9) {
           const unsigned long long fx = (unsigned long long)(long long)(cta - 70 + lane + e);
           for (int rep = 0; rep < 6; ++rep)
@@ -163,11 +165,12 @@ __global__ void k_sync(unsigned long long* recs, int E, int L, int sleep_ns, uns
       r0 += nd;
       if (nd == 0 && sleep_ns > 0) __nanosleep(sleep_ns);
     }
-  } else if (MODE >= 7) {
+  } else if (MODE == 7 || MODE == 8 || MODE == 12 || MODE == 13) {
     // M sub-accumulators per event (CTA c adds into sub c % M, each on its own
     // 256-byte line): fewer same-address atomics in a row; lane (m, c) polls
     // word c of sub m, one event per load instruction, D events per pass
-    constexpr int M = MODE == 7 ? 4 : 8;
+    constexpr int M = MODE == 7 ? 4 : MODE == 8 ? 8 : MODE == 12 ? 2 : 4;
+    constexpr int SUB = MODE >= 12 ? NS : 32;
     constexpr int D = 4;
     __shared__ unsigned long long prev[NB][M * NS];
     for (int i = lane; i < NB * M * NS; i += 32) (&prev[0][0])[i] = 0ull;
@@ -183,7 +186,7 @@ __global__ void k_sync(unsigned long long* recs, int E, int L, int sleep_ns, uns
       for (int k = 0; k < D; ++k) {
         const int r = r0 + k;
         cur[k] = 0ull;
-        if (act && r < E) cur[k] = ld_rel(recs + ((size_t)(r % NB) * M + m) * 32 + c);
+        if (act && r < E) cur[k] = ld_rel(recs + (size_t)(r % NB) * 8 * 32 + (size_t)m * SUB + c);
       }
 #pragma unroll
       for (int k = 0; k < D; ++k) {
@@ -476,16 +479,16 @@ int main(int argc, char** argv) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int E = 20000;
   unsigned long long *recs, *tout;
-  cudaMalloc(&recs, ((size_t)NB * 160 * NS + NB) * 8);
+  cudaMalloc(&recs, ((size_t)NB * 160 * NS + NB) * 8);  // >= NB * 8 * 32 words
   cudaMalloc(&tout, 160 * 8);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  const int Gs[] = {144, 145};
+  const int Gs[] = {145};
   const int Ls[] = {1, 2, 3};
   const int sleeps[] = {0, 32};
   printf("mode(events in flight) G L sleep_ns us_per_event\n");
-  for (int mode : {5})
+  for (int mode : {5, 12, 13, 7})
   for (int G : Gs) {
     if (G > sms) continue;
     for (int L : Ls)
@@ -502,7 +505,8 @@ int main(int argc, char** argv) {
                  : mode == 2 ? (void*)k_sync<2> : mode == 4 ? (void*)k_sync<4>
                  : mode == 5 ? (void*)k_sync<5> : mode == 6 ? (void*)k_sync<6>
                  : mode == 7 ? (void*)k_sync<7> : mode == 8 ? (void*)k_sync<8>
-                 : mode == 9 ? (void*)k_sync<9> : mode == 10 ? (void*)k_sync<10> : (void*)k_sync<3>;
+                 : mode == 9 ? (void*)k_sync<9> : mode == 10 ? (void*)k_sync<10>
+                 : mode == 12 ? (void*)k_sync<12> : mode == 13 ? (void*)k_sync<13> : (void*)k_sync<3>;
         cudaLaunchCooperativeKernel(fn, dim3(G), dim3(64), args, 0, 0);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
@@ -512,7 +516,7 @@ int main(int argc, char** argv) {
         fflush(stdout);
       }
   }
-  for (int cs : {2, 4}) {
+  for (int cs : {2}) {
     const int G = 144;
     for (int L : Ls)
       for (int sl : {0, 32}) {
