@@ -300,7 +300,10 @@ __global__ void __launch_bounds__(NWT * 32, 1) k_grid_epoch(GridArgs A) {
   static_assert(NRED >= 1, "no reducer warp");
   constexpr int NWC = NTC / 32;
   constexpr int NSLOT = LL + 1 + (EARLY ? 1 : 0);
-  constexpr int PUBW = 0;  // the publishing math warp
+#ifndef SYSCD_GRID_PUBW
+#define SYSCD_GRID_PUBW 2  // a warp whose scheduler it shares with a helper warp only (config 3: 5.22 -> 5.05 ms against warp 0)
+#endif
+  constexpr int PUBW = SYSCD_GRID_PUBW < NWC ? SYSCD_GRID_PUBW : 0;  // the publishing math warp
   // packed FMAs (config 3: 5.43 -> 5.38 ms with LL = 2; with LL = 3 they cost registers: 5.48 -> 5.60)
   constexpr bool F2 = SYSCD_GRID_F2 == 1 || (SYSCD_GRID_F2 == 2 && NWM == 6 && LL == 2 && BB == 1);
   static_assert(!F2 || (RR % 2 == 0 && SYSCD_GRID_CHAINS == 1), "packed FMAs: even RR, one chain");
